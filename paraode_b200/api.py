@@ -1,0 +1,446 @@
+"""Python mirror of the reference's solver API for the ParaIEKS path.
+
+Names, argument meaning and error behaviour follow proj/include/paraode/
+(parallel.hpp, ieks.hpp, prior.hpp, problems.hpp, errors.hpp); every call runs
+on the B200 through the C ABI (include/paraode_b200.h).  Matrices are
+row-major numpy float64 arrays; arrays of elements / marginals stack along
+axis 0.  There is no CPU fallback: without the CUDA library or a B200 every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _abi as A
+
+
+# ------------------------------------------------------------- errors ---
+class SolverError(RuntimeError):
+    """proj/include/paraode/errors.hpp:10-14"""
+
+
+class InvalidInputError(SolverError):
+    pass
+
+
+class DimensionError(SolverError):
+    pass
+
+
+class SingularFactorError(SolverError):
+    pass
+
+
+class LinearizationError(SolverError):
+    def __init__(self, what, time=0.0, index=0):
+        super().__init__(what)
+        self.time = time
+        self.index = index
+
+
+class ScanError(SolverError):
+    pass
+
+
+class CudaError(SolverError):
+    """No usable B200 / CUDA failure (the product path has no CPU fallback)."""
+
+
+class UnsupportedError(SolverError):
+    pass
+
+
+_ERRORS = {1: InvalidInputError, 2: DimensionError, 3: SingularFactorError,
+           4: LinearizationError, 5: ScanError, 6: CudaError, 7: UnsupportedError}
+
+
+def _raise(rc: int, st: A.Status):
+    if rc == 0:
+        return
+    cls = _ERRORS.get(rc, SolverError)
+    msg = st.msg.decode(errors="replace")
+    if cls is LinearizationError:
+        raise LinearizationError(msg, st.time, st.index)
+    raise cls(msg)
+
+
+# ------------------------------------------------------------ context ---
+class Context:
+    """One GPU + one stream + cached device workspace (pode_context)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = A.load()
+        self._h = C.c_void_p()
+        st = A.Status()
+        _raise(self._lib.pode_context_create(device, C.byref(self._h), C.byref(st)), st)
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self._lib.pode_kernel_launches(self._h))
+
+    @property
+    def stream(self) -> int:
+        return int(self._lib.pode_context_stream(self._h) or 0)
+
+    def close(self):
+        if self._h:
+            self._lib.pode_context_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context(0)
+    return _default
+
+
+def _ctx(ctx):
+    return (ctx or default_context())
+
+
+def _p(a):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"]
+    if a.dtype == np.float64:
+        return a.ctypes.data_as(A.dptr)
+    if a.dtype == np.int32:
+        return a.ctypes.data_as(A.iptr)
+    raise TypeError(a.dtype)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ------------------------------------------------------- value types ---
+@dataclass
+class FilteringElements:
+    """Array of FilteringElement (parallel.hpp:20-26)."""
+    a: np.ndarray
+    b: np.ndarray
+    c_sqrt: np.ndarray
+    eta: np.ndarray
+    j_sqrt: np.ndarray
+
+    @staticmethod
+    def empty(n, d):
+        z = np.zeros
+        return FilteringElements(z((n, d, d)), z((n, d)), z((n, d, d)), z((n, d)), z((n, d, d)))
+
+    @property
+    def count(self):
+        return self.a.shape[0]
+
+    @property
+    def state_dim(self):
+        return self.a.shape[1]
+
+    def _c(self):
+        for k in ("a", "b", "c_sqrt", "eta", "j_sqrt"):
+            setattr(self, k, _f64(getattr(self, k)))
+        return A.FilteringElements(_p(self.a), _p(self.b), _p(self.c_sqrt), _p(self.eta), _p(self.j_sqrt))
+
+
+@dataclass
+class SmoothingElements:
+    """Array of SmoothingElement (parallel.hpp:32-36)."""
+    e: np.ndarray
+    g: np.ndarray
+    l_sqrt: np.ndarray
+
+    @staticmethod
+    def empty(n, d):
+        return SmoothingElements(np.zeros((n, d, d)), np.zeros((n, d)), np.zeros((n, d, d)))
+
+    @property
+    def count(self):
+        return self.e.shape[0]
+
+    @property
+    def state_dim(self):
+        return self.e.shape[1]
+
+    def _c(self):
+        for k in ("e", "g", "l_sqrt"):
+            setattr(self, k, _f64(getattr(self, k)))
+        return A.SmoothingElements(_p(self.e), _p(self.g), _p(self.l_sqrt))
+
+
+@dataclass
+class LinearGaussianChain:
+    """init + N transitions + N affine observations (the para_rts inputs,
+    parallel.hpp:155-156).  Observation n uses obs_rows[n] rows of its
+    M-row slot (0 = vacuous); phi / q_sqrt may be shared (2-D)."""
+    init_mean: np.ndarray
+    init_cov_sqrt: np.ndarray
+    phi: np.ndarray
+    q_sqrt: np.ndarray
+    obs_rows: np.ndarray
+    h: np.ndarray
+    offset: np.ndarray
+    r_sqrt: np.ndarray
+
+    @property
+    def state_dim(self):
+        return int(np.asarray(self.init_mean).shape[0])
+
+    @property
+    def steps(self):
+        return int(np.asarray(self.obs_rows).shape[0])
+
+    def _c(self):
+        self.init_mean = _f64(self.init_mean)
+        self.init_cov_sqrt = _f64(self.init_cov_sqrt)
+        self.phi = _f64(self.phi)
+        self.q_sqrt = _f64(self.q_sqrt)
+        self.obs_rows = np.ascontiguousarray(self.obs_rows, dtype=np.int32)
+        self.h = _f64(self.h)
+        self.offset = _f64(self.offset)
+        self.r_sqrt = _f64(self.r_sqrt)
+        m = self.h.shape[1] if self.h.ndim == 3 else 0
+        return A.Chain(self.state_dim, m, self.steps, _p(self.init_mean), _p(self.init_cov_sqrt),
+                       _p(self.phi), _p(self.q_sqrt), int(self.phi.ndim == 2), int(self.q_sqrt.ndim == 2),
+                       _p(self.obs_rows), _p(self.h), _p(self.offset), _p(self.r_sqrt), A.PODE_HOST)
+
+
+@dataclass
+class RtsResult:
+    """sequential.hpp:52-56 (marginals at nodes 0..N)."""
+    filtered_mean: np.ndarray
+    filtered_cov_sqrt: np.ndarray
+    smoothed_mean: np.ndarray
+    smoothed_cov_sqrt: np.ndarray
+    combine_invocations: int = 0
+    sequential_depth: int = 0
+
+
+# ---------------------------------------------------- element operators ---
+def make_filtering_elements(chain: LinearGaussianChain, absorb_init=True, ctx=None) -> FilteringElements:
+    """make_filtering_element for every step (parallel.cpp:5-65)."""
+    c = _ctx(ctx)
+    out = FilteringElements.empty(chain.steps, chain.state_dim)
+    ch = chain._c()
+    st = A.Status()
+    _raise(c._lib.pode_make_filtering_elements(c.handle, C.byref(ch), int(absorb_init), out._c(),
+                                               C.byref(st)), st)
+    return out
+
+
+def combine_filtering(lhs: FilteringElements, rhs: FilteringElements, ctx=None) -> FilteringElements:
+    """Batched ⊗_f: out[i] = lhs[i] ⊗ rhs[i] (parallel.cpp:67-100)."""
+    c = _ctx(ctx)
+    n, d = lhs.count, lhs.state_dim
+    if rhs.count != n or rhs.state_dim != d:
+        raise DimensionError("combine_filtering: element factors must be square")
+    out = FilteringElements.empty(n, d)
+    st = A.Status()
+    _raise(c._lib.pode_combine_filtering(c.handle, n, d, lhs._c(), rhs._c(), out._c(), A.PODE_HOST,
+                                         C.byref(st)), st)
+    return out
+
+
+def make_smoothing_elements(chain: LinearGaussianChain, f_mean, f_cov_sqrt, ctx=None) -> SmoothingElements:
+    """Smoothing elements for nodes 0..N; node N terminal (parallel.cpp:112-144)."""
+    c = _ctx(ctx)
+    out = SmoothingElements.empty(chain.steps + 1, chain.state_dim)
+    ch = chain._c()
+    fm, fc = _f64(f_mean), _f64(f_cov_sqrt)
+    st = A.Status()
+    _raise(c._lib.pode_make_smoothing_elements(c.handle, C.byref(ch), _p(fm), _p(fc), out._c(), C.byref(st)), st)
+    return out
+
+
+def combine_smoothing(lhs: SmoothingElements, rhs: SmoothingElements, ctx=None) -> SmoothingElements:
+    """Batched ⊗_s (parallel.cpp:146-156)."""
+    c = _ctx(ctx)
+    n, d = lhs.count, lhs.state_dim
+    if rhs.count != n or rhs.state_dim != d:
+        raise DimensionError("combine_smoothing: element dimensions disagree")
+    out = SmoothingElements.empty(n, d)
+    st = A.Status()
+    _raise(c._lib.pode_combine_smoothing(c.handle, n, d, lhs._c(), rhs._c(), out._c(), A.PODE_HOST,
+                                         C.byref(st)), st)
+    return out
+
+
+def associative_scan_filtering(elems: FilteringElements, reverse=False, ctx=None):
+    """Inclusive scan under ⊗_f (associative_scan, parallel.hpp:136-149).
+    Returns (prefixes, (combine_invocations, sequential_depth))."""
+    c = _ctx(ctx)
+    n, d = elems.count, elems.state_dim
+    out = FilteringElements(*(np.array(x, dtype=np.float64, copy=True) for x in
+                              (elems.a, elems.b, elems.c_sqrt, elems.eta, elems.j_sqrt)))
+    st, stats = A.Status(), A.ScanStats()
+    oc = out._c()
+    _raise(c._lib.pode_scan_filtering(c.handle, n, d, oc, oc, int(reverse), A.PODE_HOST, C.byref(stats),
+                                      C.byref(st)), st)
+    return out, (stats.combine_invocations, stats.sequential_depth)
+
+
+def associative_scan_smoothing(elems: SmoothingElements, reverse=True, ctx=None):
+    c = _ctx(ctx)
+    n, d = elems.count, elems.state_dim
+    out = SmoothingElements(*(np.array(x, dtype=np.float64, copy=True) for x in (elems.e, elems.g, elems.l_sqrt)))
+    st, stats = A.Status(), A.ScanStats()
+    oc = out._c()
+    _raise(c._lib.pode_scan_smoothing(c.handle, n, d, oc, oc, int(reverse), A.PODE_HOST, C.byref(stats),
+                                      C.byref(st)), st)
+    return out, (stats.combine_invocations, stats.sequential_depth)
+
+
+def para_rts(chain: LinearGaussianChain, ctx=None) -> RtsResult:
+    """Time-parallel square-root filter + smoother (para_rts, parallel.cpp:166-209)."""
+    c = _ctx(ctx)
+    n1, d = chain.steps + 1, chain.state_dim
+    r = RtsResult(np.zeros((n1, d)), np.zeros((n1, d, d)), np.zeros((n1, d)), np.zeros((n1, d, d)))
+    ch = chain._c()
+    st, stats = A.Status(), A.ScanStats()
+    out = A.RtsOut(_p(r.filtered_mean), _p(r.filtered_cov_sqrt), _p(r.smoothed_mean), _p(r.smoothed_cov_sqrt))
+    _raise(c._lib.pode_rts(c.handle, C.byref(ch), out, C.byref(stats), C.byref(st)), st)
+    r.combine_invocations, r.sequential_depth = stats.combine_invocations, stats.sequential_depth
+    return r
+
+
+# -------------------------------------------------------------- solver ---
+@dataclass
+class IwpPrior:
+    """prior.hpp:12-18"""
+    nu: int = 1
+    dim: int = 1
+    sigma: float = 1.0
+
+    @property
+    def state_dim(self):
+        return self.dim * (self.nu + 1)
+
+
+@dataclass
+class IeksConfig:
+    """ieks.hpp:32-38"""
+    max_iterations: int = 100
+    traj_rtol: float = 1e-13
+    obj_atol: float = 1e-9
+    obj_rtol: float = 1e-6
+    linearization: str = "ek1"
+
+
+@dataclass
+class InitialValueProblem:
+    """A registered device vector field (replaces statespace.hpp:24-31)."""
+    kind: int
+    dim: int
+    t_end: float
+    y0: np.ndarray
+    params: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    name: str = ""
+
+    def _c(self):
+        self.y0 = _f64(self.y0)
+        self.params = _f64(self.params)
+        return A.Problem(self.kind, self.dim, self.t_end, _p(self.y0),
+                         _p(self.params) if self.params.size else None, int(self.params.size))
+
+
+def logistic():
+    return InitialValueProblem(1, 1, 10.0, np.array([0.01]), name="logistic")
+
+
+def rigid_body():
+    return InitialValueProblem(2, 3, 20.0, np.array([1.0, 0.0, 0.9]), name="rigidbody")
+
+
+def van_der_pol(mu=1.0):
+    return InitialValueProblem(3, 2, 6.3, np.array([2.0, 0.0]), np.array([mu]), name="vanderpol")
+
+
+def fitzhugh_nagumo(a=0.2, b=0.2, c=3.0):
+    return InitialValueProblem(4, 2, 20.0, np.array([-1.0, 1.0]), np.array([a, b, c]), name="fhn")
+
+
+def pleiades():
+    y0 = [3, 3, -1, -3, 2, -2, 2, 3, -3, 2, 0, 0, -4, 4, 0, 0, 0, 0, 0, 1.75, -1.5, 0, 0, 0, -1.25, 1, 0, 0]
+    return InitialValueProblem(5, 28, 3.0, np.array(y0, dtype=np.float64), name="pleiades")
+
+
+def affine(l, c, y0, t_end):
+    l = np.asarray(l, dtype=np.float64)
+    return InitialValueProblem(6, len(y0), t_end, np.asarray(y0, dtype=np.float64),
+                               np.concatenate([l.ravel(), np.asarray(c, dtype=np.float64)]), name="affine")
+
+
+def problem_by_name(name):
+    """problems.cpp:190-195 (+ fhn, pleiades)."""
+    table = {"logistic": logistic, "rigidbody": rigid_body, "vanderpol": van_der_pol,
+             "fhn": fitzhugh_nagumo, "pleiades": pleiades}
+    if name not in table:
+        raise InvalidInputError(f"unknown problem '{name}'")
+    return table[name]()
+
+
+def uniform_grid(t_end, steps):
+    """problems.cpp:212-221"""
+    if steps < 1 or not t_end > 0:
+        raise InvalidInputError("uniform_grid: need steps >= 1 and t_end > 0")
+    n = np.arange(steps + 1, dtype=np.float64)
+    return t_end * n / steps
+
+
+@dataclass
+class SolverReport:
+    """ieks.hpp:77-87"""
+    times: np.ndarray
+    means: np.ndarray
+    cov_sqrt: Optional[np.ndarray]
+    solution_means: np.ndarray
+    solution_covs: Optional[np.ndarray]
+    sigma_hat: float
+    iterations: int
+    objective_trace: np.ndarray
+    converged: bool
+    combine_invocations: int
+    sequential_depth: int
+
+
+def para_ieks(ivp: InitialValueProblem, prior: IwpPrior, grid: Sequence[float],
+              config: IeksConfig = IeksConfig(), want_cov=True, ctx=None) -> SolverReport:
+    """Iterated extended Kalman smoother on the B200 (para_ieks, ieks.cpp:114-217)."""
+    c = _ctx(ctx)
+    grid = _f64(grid)
+    n1 = grid.shape[0]
+    D, d = prior.state_dim, prior.dim
+    means = np.zeros((n1, D))
+    cov = np.zeros((n1, D, D)) if want_cov else None
+    sm = np.zeros((n1, d))
+    sc = np.zeros((n1, d, d)) if want_cov else None
+    trace = np.zeros(max(config.max_iterations, 1))
+    rep = A.IeksReport(_p(means), _p(cov), _p(sm), _p(sc), _p(trace), trace.shape[0], A.PODE_HOST,
+                       0, 0, 0.0, A.ScanStats())
+    pr = ivp._c()
+    prior_c = A.Prior(prior.nu, prior.dim, prior.sigma)
+    lin = {"ek1": 0, "ek0": 1}[config.linearization]
+    cfg = A.IeksConfig(config.max_iterations, config.traj_rtol, config.obj_atol, config.obj_rtol, lin)
+    st = A.Status()
+    _raise(c._lib.pode_ieks(c.handle, C.byref(pr), C.byref(prior_c), _p(grid), n1, C.byref(cfg),
+                            C.byref(rep), C.byref(st)), st)
+    return SolverReport(grid.copy(), means, cov, sm, sc, rep.sigma_hat, rep.iterations,
+                        trace[:rep.iterations].copy(), bool(rep.converged),
+                        rep.scan_stats.combine_invocations, rep.scan_stats.sequential_depth)

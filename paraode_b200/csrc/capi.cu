@@ -1,0 +1,476 @@
+// The C ABI (include/paraode_b200.h): context management, host<->device
+// staging, dispatch to the per-D engines and the mapping of device error
+// words onto the reference's exception types.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dispatch.hpp"
+#include "engine.cuh"
+#include "host_model.hpp"
+#include "ieks.cuh"
+
+namespace pode {
+
+#define PODE_DECL(n) const EngineOps* engine_ops_d##n();
+PODE_DECL(1) PODE_DECL(2) PODE_DECL(3) PODE_DECL(4) PODE_DECL(5) PODE_DECL(6) PODE_DECL(7) PODE_DECL(8)
+PODE_DECL(9) PODE_DECL(10) PODE_DECL(11) PODE_DECL(12) PODE_DECL(13) PODE_DECL(14) PODE_DECL(15) PODE_DECL(16)
+#undef PODE_DECL
+
+const EngineOps* engine_ops(int D) {
+  switch (D) {
+    case 1: return engine_ops_d1();
+    case 2: return engine_ops_d2();
+    case 3: return engine_ops_d3();
+    case 4: return engine_ops_d4();
+    case 5: return engine_ops_d5();
+    case 6: return engine_ops_d6();
+    case 7: return engine_ops_d7();
+    case 8: return engine_ops_d8();
+    case 9: return engine_ops_d9();
+    case 10: return engine_ops_d10();
+    case 11: return engine_ops_d11();
+    case 12: return engine_ops_d12();
+    case 13: return engine_ops_d13();
+    case 14: return engine_ops_d14();
+    case 15: return engine_ops_d15();
+    case 16: return engine_ops_d16();
+    default: return nullptr;
+  }
+}
+
+void reset_error(pode_context* ctx) {
+  cuda_check(cudaMemsetAsync(ctx->d_err, 0xff, sizeof(unsigned long long), ctx->stream), "reset error word");
+}
+
+unsigned long long fetch_error(pode_context* ctx) {
+  cuda_check(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             ctx->stream),
+             "fetch error word");
+  cuda_check(cudaStreamSynchronize(ctx->stream), "stream sync");
+  return *ctx->h_err;
+}
+
+namespace {
+
+const EngineOps& ops_for(int D) {
+  const EngineOps* ops = engine_ops(D);
+  if (ops == nullptr)
+    throw ApiError(PODE_ERR_UNSUPPORTED, "state dimension " + std::to_string(D) + " is outside the compiled range [" +
+                                             std::to_string(kMinD) + ", " + std::to_string(kMaxD) + "]");
+  return *ops;
+}
+
+void check_ctx(pode_context* ctx) {
+  if (ctx == nullptr) throw ApiError(PODE_ERR_INVALID_INPUT, "NULL context");
+  cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+}
+
+// Raises the device error word (if set) as the matching ApiError.
+void raise_device_error(pode_context* ctx, const char* stage, int scan_code = 0) {
+  const unsigned long long key = fetch_error(ctx);
+  if (key == ~0ull) return;
+  const int code = int(key & 0xff);
+  const int64_t idx = int64_t(key >> 8);
+  if (scan_code) {
+    ApiError e(PODE_ERR_SCAN,
+               std::string("associative_scan: combine failed on elements [") + std::to_string(idx) + ", " +
+                   std::to_string(idx) + "]: " + stage + ": triangular factor is singular",
+               idx);
+    throw e;
+  }
+  if (code == kErrLinearization)
+    throw ApiError(PODE_ERR_LINEARIZATION, std::string(stage) + ": vector field evaluation is not finite", idx);
+  if (code == kErrInvalid) throw ApiError(PODE_ERR_INVALID_INPUT, std::string(stage) + ": non-finite input", idx);
+  throw ApiError(PODE_ERR_SINGULAR_FACTOR, std::string(stage) + ": triangular factor is singular", idx);
+}
+
+template <typename F>
+int guarded(pode_status* st, F&& f) {
+  if (st) {
+    std::memset(st, 0, sizeof(*st));
+    st->index = -1;
+  }
+  try {
+    f();
+    return PODE_OK;
+  } catch (const ApiError& e) {
+    if (st) {
+      st->code = e.code;
+      st->index = e.index;
+      st->lo = st->hi = e.index;
+      st->time = e.time;
+      st->iteration = e.iteration;
+      std::strncpy(st->msg, e.what(), sizeof(st->msg) - 1);
+    }
+    return e.code;
+  } catch (const std::exception& e) {
+    if (st) {
+      st->code = PODE_ERR_CUDA;
+      std::strncpy(st->msg, e.what(), sizeof(st->msg) - 1);
+    }
+    return PODE_ERR_CUDA;
+  }
+}
+
+// Copies host arrays into a tagged workspace buffer (or passes device
+// pointers through).
+template <typename T>
+T* stage_in(pode_context* ctx, const std::string& tag, const T* src, size_t count, bool device) {
+  if (src == nullptr) return nullptr;
+  if (device) return const_cast<T*>(src);
+  T* d = ctx->ws.arr<T>(tag, count);
+  cuda_check(cudaMemcpyAsync(d, src, sizeof(T) * count, cudaMemcpyHostToDevice, ctx->stream), tag.c_str());
+  return d;
+}
+
+template <typename T>
+void stage_out(pode_context* ctx, T* dst, const T* dev, size_t count, bool device) {
+  if (dst == nullptr || device) return;
+  cuda_check(cudaMemcpyAsync(dst, dev, sizeof(T) * count, cudaMemcpyDeviceToHost, ctx->stream), "copy out");
+}
+
+void check_dims(int D, int64_t count) {
+  if (D < 1) throw ApiError(PODE_ERR_DIMENSION, "state dimension must be >= 1");
+  if (count < 0) throw ApiError(PODE_ERR_DIMENSION, "negative count");
+}
+
+DevChain stage_chain(pode_context* ctx, const pode_chain* c) {
+  if (c == nullptr) throw ApiError(PODE_ERR_INVALID_INPUT, "NULL chain");
+  if (c->steps < 1) throw ApiError(PODE_ERR_DIMENSION, "smoother: need N >= 1 aligned transitions and observations");
+  const int D = c->state_dim, M = c->obs_rows_max;
+  if (D < 1 || M < 0 || M > D) throw ApiError(PODE_ERR_DIMENSION, "chain: need 0 <= obs_rows_max <= state_dim");
+  const bool dev = c->location == PODE_DEVICE;
+  const int64_t N = c->steps;
+  const int Mm = std::max(M, 1);
+  if (!dev) {
+    for (int64_t n = 0; n < N; ++n)
+      if (c->obs_rows[n] < 0 || c->obs_rows[n] > M)
+        throw ApiError(PODE_ERR_DIMENSION, "smoother: observation dimensions disagree with the state", n);
+  }
+  DevChain ch;
+  ch.D = D;
+  ch.M = Mm;
+  ch.N = N;
+  ch.init_mean = stage_in(ctx, "ch_init_mean", c->init_mean, D, dev);
+  ch.init_cov = stage_in(ctx, "ch_init_cov", c->init_cov_sqrt, size_t(D) * D, dev);
+  ch.phi_shared = c->phi_shared;
+  ch.q_shared = c->q_shared;
+  ch.phi = stage_in(ctx, "ch_phi", c->phi, size_t(c->phi_shared ? 1 : N) * D * D, dev);
+  ch.q = stage_in(ctx, "ch_q", c->q_sqrt, size_t(c->q_shared ? 1 : N) * D * D, dev);
+  ch.obs_rows = stage_in(ctx, "ch_rows", c->obs_rows, size_t(N), dev);
+  if (M == 0) {
+    // no observation rows anywhere: give the kernels valid zero buffers
+    double* z = ctx->ws.arr<double>("ch_zero", size_t(N) * (D + 2));
+    cuda_check(cudaMemsetAsync(z, 0, sizeof(double) * size_t(N) * (D + 2), ctx->stream), "zero");
+    ch.h = z;
+    ch.off = z + size_t(N) * D;
+    ch.r = z + size_t(N) * (D + 1);
+  } else {
+    ch.h = stage_in(ctx, "ch_h", c->h, size_t(N) * M * D, dev);
+    ch.off = stage_in(ctx, "ch_off", c->offset, size_t(N) * M, dev);
+    ch.r = stage_in(ctx, "ch_r", c->r_sqrt, size_t(N) * M * M, dev);
+  }
+  return ch;
+}
+
+FEd fe_view(const pode_filtering_elements& e) { return FEd{e.a, e.b, e.c_sqrt, e.eta, e.j_sqrt}; }
+SEd se_view(const pode_smoothing_elements& e) { return SEd{e.e, e.g, e.l_sqrt}; }
+
+FEd stage_fe(pode_context* ctx, const std::string& tag, const pode_filtering_elements& e, int64_t n, int D,
+             bool dev, bool copy) {
+  if (dev) return fe_view(e);
+  const size_t mm = size_t(n) * D * D, vv = size_t(n) * D;
+  double* base = ctx->ws.arr<double>(tag, 3 * mm + 2 * vv);
+  FEd d{base, base + mm, base + mm + vv, base + 2 * mm + vv, base + 2 * mm + 2 * vv};
+  if (copy) {
+    cuda_check(cudaMemcpyAsync(d.a, e.a, sizeof(double) * mm, cudaMemcpyHostToDevice, ctx->stream), "a");
+    cuda_check(cudaMemcpyAsync(d.b, e.b, sizeof(double) * vv, cudaMemcpyHostToDevice, ctx->stream), "b");
+    cuda_check(cudaMemcpyAsync(d.c, e.c_sqrt, sizeof(double) * mm, cudaMemcpyHostToDevice, ctx->stream), "c");
+    cuda_check(cudaMemcpyAsync(d.eta, e.eta, sizeof(double) * vv, cudaMemcpyHostToDevice, ctx->stream), "eta");
+    cuda_check(cudaMemcpyAsync(d.j, e.j_sqrt, sizeof(double) * mm, cudaMemcpyHostToDevice, ctx->stream), "j");
+  }
+  return d;
+}
+
+void unstage_fe(pode_context* ctx, const pode_filtering_elements& e, const FEd& d, int64_t n, int D, bool dev) {
+  if (dev) return;
+  const size_t mm = size_t(n) * D * D, vv = size_t(n) * D;
+  stage_out(ctx, e.a, d.a, mm, false);
+  stage_out(ctx, e.b, d.b, vv, false);
+  stage_out(ctx, e.c_sqrt, d.c, mm, false);
+  stage_out(ctx, e.eta, d.eta, vv, false);
+  stage_out(ctx, e.j_sqrt, d.j, mm, false);
+}
+
+SEd stage_se(pode_context* ctx, const std::string& tag, const pode_smoothing_elements& e, int64_t n, int D,
+             bool dev, bool copy) {
+  if (dev) return se_view(e);
+  const size_t mm = size_t(n) * D * D, vv = size_t(n) * D;
+  double* base = ctx->ws.arr<double>(tag, 2 * mm + vv);
+  SEd d{base, base + mm, base + mm + vv};
+  if (copy) {
+    cuda_check(cudaMemcpyAsync(d.e, e.e, sizeof(double) * mm, cudaMemcpyHostToDevice, ctx->stream), "e");
+    cuda_check(cudaMemcpyAsync(d.g, e.g, sizeof(double) * vv, cudaMemcpyHostToDevice, ctx->stream), "g");
+    cuda_check(cudaMemcpyAsync(d.l, e.l_sqrt, sizeof(double) * mm, cudaMemcpyHostToDevice, ctx->stream), "l");
+  }
+  return d;
+}
+
+void unstage_se(pode_context* ctx, const pode_smoothing_elements& e, const SEd& d, int64_t n, int D, bool dev) {
+  if (dev) return;
+  const size_t mm = size_t(n) * D * D, vv = size_t(n) * D;
+  stage_out(ctx, e.e, d.e, mm, false);
+  stage_out(ctx, e.g, d.g, vv, false);
+  stage_out(ctx, e.l_sqrt, d.l, mm, false);
+}
+
+void sync(pode_context* ctx) { cuda_check(cudaStreamSynchronize(ctx->stream), "stream sync"); }
+
+}  // namespace
+}  // namespace pode
+
+using namespace pode;
+
+extern "C" {
+
+int pode_context_create(int32_t device, pode_context** out, pode_status* status) {
+  return guarded(status, [&] {
+    if (out == nullptr) throw ApiError(PODE_ERR_INVALID_INPUT, "NULL out");
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+      throw ApiError(PODE_ERR_CUDA, "no CUDA device visible (paraode_b200 has no CPU fallback)");
+    if (device < 0 || device >= count) throw ApiError(PODE_ERR_CUDA, "device index out of range");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop{};
+    cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10)
+      throw ApiError(PODE_ERR_CUDA, std::string("paraode_b200 is built for sm_100a (B200); found ") + prop.name);
+    auto* ctx = new pode_context();
+    ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
+    try {
+      cuda_check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+      cuda_check(cudaMalloc(&ctx->d_err, sizeof(unsigned long long)), "error word");
+      cuda_check(cudaMallocHost(&ctx->h_err, sizeof(unsigned long long)), "pinned");
+      cuda_check(cudaMallocHost(&ctx->h_scalars, sizeof(double) * 16), "pinned");
+      reset_error(ctx);
+      sync(ctx);
+    } catch (...) {
+      pode_context_destroy(ctx);
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+void pode_context_destroy(pode_context* ctx) {
+  if (ctx == nullptr) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->ws.bufs.clear();
+  if (ctx->d_err) cudaFree(ctx->d_err);
+  if (ctx->h_err) cudaFreeHost(ctx->h_err);
+  if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int32_t pode_max_state_dim(void) { return kMaxD; }
+
+int64_t pode_kernel_launches(const pode_context* ctx) { return ctx ? ctx->launches : 0; }
+
+void* pode_context_stream(pode_context* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int pode_combine_filtering(pode_context* ctx, int64_t count, int32_t D, pode_filtering_elements lhs,
+                           pode_filtering_elements rhs, pode_filtering_elements out, int32_t location,
+                           pode_status* status) {
+  return guarded(status, [&] {
+    check_ctx(ctx);
+    check_dims(D, count);
+    if (count == 0) return;
+    const auto& ops = ops_for(D);
+    const bool dev = location == PODE_DEVICE;
+    const FEd l = stage_fe(ctx, "cf_l", lhs, count, D, dev, true);
+    const FEd r = stage_fe(ctx, "cf_r", rhs, count, D, dev, true);
+    const FEd o = stage_fe(ctx, "cf_o", out, count, D, dev, false);
+    reset_error(ctx);
+    ops.combine_filtering(ctx, count, l, r, o);
+    unstage_fe(ctx, out, o, count, D, dev);
+    raise_device_error(ctx, "combine_filtering: combination factor");
+  });
+}
+
+int pode_combine_smoothing(pode_context* ctx, int64_t count, int32_t D, pode_smoothing_elements lhs,
+                           pode_smoothing_elements rhs, pode_smoothing_elements out, int32_t location,
+                           pode_status* status) {
+  return guarded(status, [&] {
+    check_ctx(ctx);
+    check_dims(D, count);
+    if (count == 0) return;
+    const auto& ops = ops_for(D);
+    const bool dev = location == PODE_DEVICE;
+    const SEd l = stage_se(ctx, "cs_l", lhs, count, D, dev, true);
+    const SEd r = stage_se(ctx, "cs_r", rhs, count, D, dev, true);
+    const SEd o = stage_se(ctx, "cs_o", out, count, D, dev, false);
+    reset_error(ctx);
+    ops.combine_smoothing(ctx, count, l, r, o);
+    unstage_se(ctx, out, o, count, D, dev);
+    raise_device_error(ctx, "combine_smoothing");
+  });
+}
+
+int pode_make_filtering_elements(pode_context* ctx, const pode_chain* chain, int32_t absorb_init,
+                                 pode_filtering_elements out, pode_status* status) {
+  return guarded(status, [&] {
+    check_ctx(ctx);
+    const DevChain ch = stage_chain(ctx, chain);
+    const auto& ops = ops_for(ch.D);
+    const bool dev = chain->location == PODE_DEVICE;
+    const FEd o = stage_fe(ctx, "mf_o", out, ch.N, ch.D, dev, false);
+    reset_error(ctx);
+    ops.make_filtering(ctx, ch, absorb_init, o);
+    unstage_fe(ctx, out, o, ch.N, ch.D, dev);
+    raise_device_error(ctx, "make_filtering_element: innovation covariance");
+  });
+}
+
+int pode_make_smoothing_elements(pode_context* ctx, const pode_chain* chain, const double* f_mean,
+                                 const double* f_cov_sqrt, pode_smoothing_elements out, pode_status* status) {
+  return guarded(status, [&] {
+    check_ctx(ctx);
+    const DevChain ch = stage_chain(ctx, chain);
+    const auto& ops = ops_for(ch.D);
+    const bool dev = chain->location == PODE_DEVICE;
+    const int D = ch.D;
+    const int64_t n1 = ch.N + 1;
+    const double* fm = stage_in(ctx, "ms_fm", f_mean, size_t(n1) * D, dev);
+    const double* fc = stage_in(ctx, "ms_fc", f_cov_sqrt, size_t(n1) * D * D, dev);
+    const SEd o = stage_se(ctx, "ms_o", out, n1, D, dev, false);
+    reset_error(ctx);
+    ops.make_smoothing(ctx, ch, fm, fc, o);
+    unstage_se(ctx, out, o, n1, D, dev);
+    raise_device_error(ctx, "make_smoothing_element: predicted covariance");
+  });
+}
+
+int pode_scan_filtering(pode_context* ctx, int64_t count, int32_t D, pode_filtering_elements in,
+                        pode_filtering_elements out, int32_t reverse, int32_t location, pode_scan_stats* stats,
+                        pode_status* status) {
+  return guarded(status, [&] {
+    check_ctx(ctx);
+    check_dims(D, count);
+    if (stats) *stats = {0, 0};
+    if (count == 0) return;
+    const auto& ops = ops_for(D);
+    const bool dev = location == PODE_DEVICE;
+    const FEd i = stage_fe(ctx, "sf_io", in, count, D, dev, true);
+    const FEd o = dev ? fe_view(out) : i;
+    reset_error(ctx);
+    ScanTally t;
+    ops.scan_filtering(ctx, count, i, o, reverse != 0, &t);
+    unstage_fe(ctx, out, o, count, D, dev);
+    raise_device_error(ctx, "combine_filtering: combination factor", 1);
+    if (stats) *stats = {t.combines, t.depth};
+  });
+}
+
+int pode_scan_smoothing(pode_context* ctx, int64_t count, int32_t D, pode_smoothing_elements in,
+                        pode_smoothing_elements out, int32_t reverse, int32_t location, pode_scan_stats* stats,
+                        pode_status* status) {
+  return guarded(status, [&] {
+    check_ctx(ctx);
+    check_dims(D, count);
+    if (stats) *stats = {0, 0};
+    if (count == 0) return;
+    const auto& ops = ops_for(D);
+    const bool dev = location == PODE_DEVICE;
+    const SEd i = stage_se(ctx, "ss_io", in, count, D, dev, true);
+    const SEd o = dev ? se_view(out) : i;
+    reset_error(ctx);
+    ScanTally t;
+    ops.scan_smoothing(ctx, count, i, o, reverse != 0, &t);
+    unstage_se(ctx, out, o, count, D, dev);
+    raise_device_error(ctx, "combine_smoothing", 1);
+    if (stats) *stats = {t.combines, t.depth};
+  });
+}
+
+int pode_rts(pode_context* ctx, const pode_chain* chain, pode_rts_out out, pode_scan_stats* stats,
+             pode_status* status) {
+  return guarded(status, [&] {
+    check_ctx(ctx);
+    const DevChain ch = stage_chain(ctx, chain);
+    const auto& ops = ops_for(ch.D);
+    const bool dev = chain->location == PODE_DEVICE;
+    const int D = ch.D;
+    const int64_t n1 = ch.N + 1;
+    double* fm = dev && out.filtered_mean ? out.filtered_mean : ctx->ws.arr<double>("rts_fm", n1 * D);
+    double* fc = dev && out.filtered_cov_sqrt ? out.filtered_cov_sqrt : ctx->ws.arr<double>("rts_fc", n1 * D * D);
+    double* sm = dev && out.smoothed_mean ? out.smoothed_mean : ctx->ws.arr<double>("rts_sm", n1 * D);
+    double* sc = dev && out.smoothed_cov_sqrt ? out.smoothed_cov_sqrt : ctx->ws.arr<double>("rts_sc", n1 * D * D);
+    reset_error(ctx);
+    ScanTally t;
+    ops.rts(ctx, ch, fm, fc, sm, sc, &t);
+    if (!dev) {
+      stage_out(ctx, out.filtered_mean, fm, size_t(n1) * D, false);
+      stage_out(ctx, out.filtered_cov_sqrt, fc, size_t(n1) * D * D, false);
+      stage_out(ctx, out.smoothed_mean, sm, size_t(n1) * D, false);
+      stage_out(ctx, out.smoothed_cov_sqrt, sc, size_t(n1) * D * D, false);
+    }
+    raise_device_error(ctx, "para_rts");
+    if (stats) *stats = {t.combines, t.depth};
+  });
+}
+
+int pode_ieks(pode_context* ctx, const pode_problem* problem, const pode_prior* prior, const double* grid,
+              int64_t n_nodes, const pode_ieks_config* config, pode_ieks_report* report, pode_status* status) {
+  return guarded(status, [&] {
+    check_ctx(ctx);
+    if (problem == nullptr || prior == nullptr || grid == nullptr || config == nullptr || report == nullptr)
+      throw ApiError(PODE_ERR_INVALID_INPUT, "ieks: NULL argument");
+    const host::Problem p = host::resolve_problem(*problem);
+    if (p.dim != prior->dim) throw ApiError(PODE_ERR_DIMENSION, "ieks: problem and prior dimensions disagree");
+    if (config->max_iterations < 1) throw ApiError(PODE_ERR_INVALID_INPUT, "ieks: max_iterations must be at least 1");
+    if (prior->nu < 1 || prior->dim < 1) throw ApiError(PODE_ERR_INVALID_INPUT, "IwpPrior: need nu >= 1 and dim >= 1");
+    if (!(prior->sigma >= 0.0) || !std::isfinite(prior->sigma))
+      throw ApiError(PODE_ERR_INVALID_INPUT, "IwpPrior: sigma must be finite and nonnegative");
+    if (n_nodes < 2) throw ApiError(PODE_ERR_INVALID_INPUT, "discretize: grid needs at least two nodes");
+    if (grid[0] != 0.0) throw ApiError(PODE_ERR_INVALID_INPUT, "discretize: grid must start at t = 0");
+    for (int64_t n = 0; n + 1 < n_nodes; ++n)
+      if (!(grid[n + 1] > grid[n])) throw ApiError(PODE_ERR_INVALID_INPUT, "discretize: grid must be strictly increasing");
+    const int D = prior->dim * (prior->nu + 1);
+    const auto& ops = ops_for(D);
+    const bool dev = report->location == PODE_DEVICE;
+    const int d = prior->dim;
+    double* means = dev ? report->means : (report->means ? ctx->ws.arr<double>("out_means", n_nodes * D) : nullptr);
+    double* cov = dev ? report->cov_sqrt : (report->cov_sqrt ? ctx->ws.arr<double>("out_cov", n_nodes * D * D) : nullptr);
+    double* sm = dev ? report->solution_means
+                     : (report->solution_means ? ctx->ws.arr<double>("out_sm", n_nodes * d) : nullptr);
+    double* sc = dev ? report->solution_covs
+                     : (report->solution_covs ? ctx->ws.arr<double>("out_sc", n_nodes * d * d) : nullptr);
+    IeksResult r;
+    ops.ieks(ctx, p, *prior, grid, n_nodes, *config, means, cov, sm, sc, &r);
+    if (!dev) {
+      stage_out(ctx, report->means, means, size_t(n_nodes) * D, false);
+      stage_out(ctx, report->cov_sqrt, cov, size_t(n_nodes) * D * D, false);
+      stage_out(ctx, report->solution_means, sm, size_t(n_nodes) * d, false);
+      stage_out(ctx, report->solution_covs, sc, size_t(n_nodes) * d * d, false);
+    }
+    raise_device_error(ctx, "ieks: calibration");
+    report->iterations = r.iterations;
+    report->converged = r.converged ? 1 : 0;
+    report->sigma_hat = r.sigma_hat;
+    report->scan_stats = {r.stats.combines, r.stats.depth};
+    if (report->objective_trace)
+      for (int k = 0; k < int(r.trace.size()) && k < report->trace_capacity; ++k)
+        report->objective_trace[k] = r.trace[k];
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// Host-side context: one GPU, one stream, a grow-only device workspace and
+// the device error word.  Shared by the C ABI (capi.cu) and the per-D
+// engines (engine.cuh).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/paraode_b200.h"
+
+namespace pode {
+
+struct DevError;
+
+// Error raised on the host side of the ABI; carries a pode_code.
+struct ApiError : std::runtime_error {
+  ApiError(int c, const std::string& m, int64_t idx = -1, double t = 0.0, int it = 0)
+      : std::runtime_error(m), code(c), index(idx), time(t), iteration(it) {}
+  int code;
+  int64_t index;
+  double time;
+  int iteration;
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw ApiError(PODE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct Workspace {
+  struct Buf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+  };
+  std::map<std::string, Buf> bufs;
+  void* get(const std::string& tag, size_t bytes) {
+    Buf& b = bufs[tag];
+    if (b.bytes < bytes) {
+      if (b.ptr) cudaFree(b.ptr);
+      b.ptr = nullptr;
+      b.bytes = 0;
+      const size_t alloc = bytes < 256 ? 256 : bytes;
+      cuda_check(cudaMalloc(&b.ptr, alloc), ("workspace alloc " + tag).c_str());
+      b.bytes = alloc;
+    }
+    return b.ptr;
+  }
+  template <typename T>
+  T* arr(const std::string& tag, size_t count) {
+    return static_cast<T*>(get(tag, count * sizeof(T)));
+  }
+  ~Workspace() {
+    for (auto& kv : bufs)
+      if (kv.second.ptr) cudaFree(kv.second.ptr);
+  }
+};
+
+}  // namespace pode
+
+struct pode_context {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  pode::Workspace ws;
+  unsigned long long* d_err = nullptr;  // device error word (DevError)
+  unsigned long long* h_err = nullptr;  // pinned mirror
+  double* h_scalars = nullptr;          // pinned scalars (reductions)
+  int64_t launches = 0;
+};
+
+namespace pode {
+
+inline void note_launch(pode_context* ctx, const char* what) {
+  ctx->launches += 1;
+  cuda_check(cudaGetLastError(), what);
+}
+
+// Resets the device error word (before a stage) / reads it back (after).
+void reset_error(pode_context* ctx);
+// Returns the packed key ((index << 8) | code), ~0ull when clean. Syncs.
+unsigned long long fetch_error(pode_context* ctx);
+
+}  // namespace pode

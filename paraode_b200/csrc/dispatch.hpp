@@ -1,0 +1,35 @@
+// Runtime dispatch from the state dimension D to the compiled engine.
+#pragma once
+
+#include "context.hpp"
+
+namespace pode {
+
+struct FEd;
+struct SEd;
+struct DevChain;
+struct ScanTally;
+struct IeksResult;
+namespace host {
+struct Problem;
+}
+
+struct EngineOps {
+  int D;
+  void (*combine_filtering)(pode_context*, int64_t, const FEd&, const FEd&, const FEd&);
+  void (*combine_smoothing)(pode_context*, int64_t, const SEd&, const SEd&, const SEd&);
+  void (*make_filtering)(pode_context*, const DevChain&, int, const FEd&);
+  void (*make_smoothing)(pode_context*, const DevChain&, const double*, const double*, const SEd&);
+  void (*scan_filtering)(pode_context*, int64_t, const FEd&, const FEd&, bool, ScanTally*);
+  void (*scan_smoothing)(pode_context*, int64_t, const SEd&, const SEd&, bool, ScanTally*);
+  void (*rts)(pode_context*, const DevChain&, double*, double*, double*, double*, ScanTally*);
+  void (*ieks)(pode_context*, const host::Problem&, const pode_prior&, const double*, int64_t,
+               const pode_ieks_config&, double*, double*, double*, double*, IeksResult*);
+};
+
+constexpr int kMinD = 1;
+constexpr int kMaxD = 16;
+
+const EngineOps* engine_ops(int D);  // nullptr when D is not compiled
+
+}  // namespace pode

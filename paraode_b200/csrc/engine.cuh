@@ -1,0 +1,481 @@
+// Per-state-dimension engine: element kernels, the chunked associative scans
+// and the smoother built from them.  Instantiated once per D in inst_*.cu.
+//
+// Scan design (replaces associative_scan / scan_in_place,
+// proj/include/paraode/parallel.hpp:86-149): a reduce-then-scan over chunks.
+// Each group of D lanes folds one chunk of L consecutive elements in time
+// order (reduce), the chunk aggregates are scanned recursively with the same
+// kernels, and each group re-folds its chunk from its exclusive carry
+// (downsweep).  The combination tree depends only on (n, L), so results are
+// bitwise reproducible run to run; work is <= 2n combines.
+#pragma once
+
+#include <algorithm>
+#include <vector>
+
+#include "context.hpp"
+#include "ops.cuh"
+
+namespace pode {
+
+constexpr int kWarpsPerBlock = 4;
+constexpr int kThreads = 32 * kWarpsPerBlock;
+
+struct FEd {  // device filtering-element arrays
+  double *a, *b, *c, *eta, *j;
+};
+struct SEd {
+  double *e, *g, *l;
+};
+
+struct DevChain {  // device view of pode_chain
+  int D, M;
+  int64_t N;
+  const double* init_mean;
+  const double* init_cov;
+  const double* phi;
+  const double* q;
+  int phi_shared, q_shared;
+  const int32_t* obs_rows;
+  const double* h;
+  const double* off;
+  const double* r;
+};
+
+struct ScanTally {
+  int64_t combines = 0;
+  int64_t depth = 0;
+};
+
+template <int D>
+constexpr size_t smem_bytes() {
+  return sizeof(double) * kWarpsPerBlock * Grp<D>::kSlots * Scratch<D>::kDoubles;
+}
+
+template <int D>
+__device__ __forceinline__ Grp<D> make_group(double* smem) {
+  const int warp = threadIdx.x >> 5;
+  return Grp<D>::make(smem + warp * Grp<D>::kSlots * Scratch<D>::kDoubles);
+}
+
+// Global group index of this lane's group.
+template <int D>
+__device__ __forceinline__ int64_t group_index(const Grp<D>& g) {
+  const int warp = threadIdx.x >> 5;
+  return (static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + warp) * Grp<D>::kPerWarp + g.gw;
+}
+
+template <int D>
+inline unsigned blocks_for(int64_t groups) {
+  const int64_t per_block = int64_t(kWarpsPerBlock) * Grp<D>::kPerWarp;
+  return static_cast<unsigned>((groups + per_block - 1) / per_block);
+}
+
+// ------------------------------------------------------------ load/store ---
+template <int D>
+__device__ __forceinline__ Rw<D> ld_row(const double* base, int64_t i, int r, bool ok) {
+  Rw<D> o;
+  const double* p = base + (i * D + r) * D;
+#pragma unroll
+  for (int j = 0; j < D; ++j) o[j] = ok ? p[j] : 0.0;
+  return o;
+}
+template <int D>
+__device__ __forceinline__ void st_row(double* base, int64_t i, int r, bool ok, const Rw<D>& x) {
+  if (!ok) return;
+  double* p = base + (i * D + r) * D;
+#pragma unroll
+  for (int j = 0; j < D; ++j) p[j] = x[j];
+}
+template <int D>
+__device__ __forceinline__ double ld_ent(const double* base, int64_t i, int r, bool ok) {
+  return ok ? base[i * D + r] : 0.0;
+}
+template <int D>
+__device__ __forceinline__ void st_ent(double* base, int64_t i, int r, bool ok, double x) {
+  if (ok) base[i * D + r] = x;
+}
+
+template <int D>
+struct FOps {
+  using El = FEl<D>;
+  using Arr = FEd;
+  __device__ static El load(const Arr& x, int64_t i, int r, bool ok) {
+    El e;
+    e.a = ld_row<D>(x.a, i, r, ok);
+    e.b = ld_ent<D>(x.b, i, r, ok);
+    e.c = ld_row<D>(x.c, i, r, ok);
+    e.eta = ld_ent<D>(x.eta, i, r, ok);
+    e.j = ld_row<D>(x.j, i, r, ok);
+    return e;
+  }
+  __device__ static void store(const Arr& x, int64_t i, int r, bool ok, const El& e) {
+    st_row<D>(x.a, i, r, ok, e.a);
+    st_ent<D>(x.b, i, r, ok, e.b);
+    st_row<D>(x.c, i, r, ok, e.c);
+    st_ent<D>(x.eta, i, r, ok, e.eta);
+    st_row<D>(x.j, i, r, ok, e.j);
+  }
+  __device__ static bool combine(const Grp<D>& g, const El& l, const El& rr, El& out) {
+    return combine_filtering<D>(g, l, rr, out);
+  }
+  __device__ static El select(bool take_a, const El& a, const El& b) {
+    El o;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      o.a[j] = take_a ? a.a[j] : b.a[j];
+      o.c[j] = take_a ? a.c[j] : b.c[j];
+      o.j[j] = take_a ? a.j[j] : b.j[j];
+    }
+    o.b = take_a ? a.b : b.b;
+    o.eta = take_a ? a.eta : b.eta;
+    return o;
+  }
+};
+
+template <int D>
+struct SOps {
+  using El = SEl<D>;
+  using Arr = SEd;
+  __device__ static El load(const Arr& x, int64_t i, int r, bool ok) {
+    El e;
+    e.e = ld_row<D>(x.e, i, r, ok);
+    e.g = ld_ent<D>(x.g, i, r, ok);
+    e.l = ld_row<D>(x.l, i, r, ok);
+    return e;
+  }
+  __device__ static void store(const Arr& x, int64_t i, int r, bool ok, const El& e) {
+    st_row<D>(x.e, i, r, ok, e.e);
+    st_ent<D>(x.g, i, r, ok, e.g);
+    st_row<D>(x.l, i, r, ok, e.l);
+  }
+  __device__ static bool combine(const Grp<D>& g, const El& l, const El& rr, El& out) {
+    return combine_smoothing<D>(g, l, rr, out);
+  }
+  __device__ static El select(bool take_a, const El& a, const El& b) {
+    El o;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      o.e[j] = take_a ? a.e[j] : b.e[j];
+      o.l[j] = take_a ? a.l[j] : b.l[j];
+    }
+    o.g = take_a ? a.g : b.g;
+    return o;
+  }
+};
+
+// ------------------------------------------------------ batched combines ---
+template <int D, class Op>
+__global__ void __launch_bounds__(kThreads) k_combine(int64_t count, typename Op::Arr lhs,
+                                                      typename Op::Arr rhs, typename Op::Arr out,
+                                                      DevError* err) {
+  extern __shared__ double smem[];
+  const Grp<D> g = make_group<D>(smem);
+  const int64_t i = group_index<D>(g);
+  const bool ok = g.real() && i < count;
+  const auto l = Op::load(lhs, i, g.r, ok);
+  const auto rr = Op::load(rhs, i, g.r, ok);
+  typename Op::El o;
+  const bool good = Op::combine(g, l, rr, o);
+  if (ok && g.r == 0 && !good) raise_error(err, i, kErrSingular);
+  Op::store(out, i, g.r, ok, o);
+}
+
+// ------------------------------------------------------------- observation ---
+template <int D>
+__device__ __forceinline__ Obs<D, D> load_obs(const DevChain& ch, int64_t i, int r, bool ok) {
+  Obs<D, D> o;
+  const int m = ok ? ch.obs_rows[i] : 0;
+  o.m = m;
+  const int M = ch.M;
+  const bool real_row = ok && r < m;
+#pragma unroll
+  for (int j = 0; j < D; ++j) o.h[j] = real_row ? ch.h[(i * M + r) * D + j] : 0.0;
+  o.off = real_row ? ch.off[i * M + r] : 0.0;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    if (real_row)
+      o.r[j] = (j < m) ? ch.r[(i * M + r) * M + j] : 0.0;
+    else
+      o.r[j] = (j == r) ? 1.0 : 0.0;  // unit-noise dummy row
+  }
+  return o;
+}
+
+template <int D>
+__device__ __forceinline__ Rw<D> chain_phi(const DevChain& ch, int64_t i, int r, bool ok) {
+  return ld_row<D>(ch.phi, ch.phi_shared ? 0 : i, r, ok);
+}
+template <int D>
+__device__ __forceinline__ Rw<D> chain_q(const DevChain& ch, int64_t i, int r, bool ok) {
+  return ld_row<D>(ch.q, ch.q_shared ? 0 : i, r, ok);
+}
+
+// make_filtering_element for every step (parallel.cpp:5-65).
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_make_filtering(DevChain ch, int absorb_init, FEd out,
+                                                             DevError* err) {
+  extern __shared__ double smem[];
+  const Grp<D> g = make_group<D>(smem);
+  const int64_t i = group_index<D>(g);
+  const bool ok = g.real() && i < ch.N;
+  const Rw<D> phi = chain_phi<D>(ch, i, g.r, ok);
+  const Rw<D> q = chain_q<D>(ch, i, g.r, ok);
+  const Obs<D, D> o = load_obs<D>(ch, i, g.r, ok);
+  FEl<D> el;
+  bool good;
+  // Warp-uniform: every group evaluates both forms, the first step keeps
+  // the init-absorbing one.
+  FEl<D> e_first;
+  Gauss<D> init;
+  init.m = ok ? ch.init_mean[g.r] : 0.0;
+  init.c = ld_row<D>(ch.init_cov, 0, g.r, ok);
+  const bool good_first = first_filtering_element<D, D>(g, init, phi, q, o, e_first);
+  const bool good_int = filtering_element<D, D>(g, phi, q, o, el);
+  const bool first = absorb_init && i == 0;
+  el = FOps<D>::select(first, e_first, el);
+  good = first ? good_first : good_int;
+  if (ok && g.r == 0 && !good) raise_error(err, i, kErrSingular);
+  FOps<D>::store(out, i, g.r, ok, el);
+}
+
+// Smoothing elements for nodes 0..N (parallel.cpp:112-144).
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_make_smoothing(DevChain ch, const double* fm,
+                                                             const double* fc, SEd out, DevError* err) {
+  extern __shared__ double smem[];
+  const Grp<D> g = make_group<D>(smem);
+  const int64_t i = group_index<D>(g);
+  const bool ok = g.real() && i <= ch.N;
+  const bool terminal = i == ch.N;
+  const bool ok_t = ok && !terminal;
+  Gauss<D> f;
+  f.m = ld_ent<D>(fm, i, g.r, ok);
+  f.c = ld_row<D>(fc, i, g.r, ok);
+  const Rw<D> phi = chain_phi<D>(ch, i, g.r, ok_t);
+  const Rw<D> q = chain_q<D>(ch, i, g.r, ok_t);
+  SEl<D> el;
+  const bool good = smoothing_element<D>(g, f, phi, q, el);
+  el = SOps<D>::select(terminal, terminal_smoothing_element<D>(f), el);
+  if (ok_t && g.r == 0 && !good) raise_error(err, i, kErrSingular);
+  SOps<D>::store(out, i, g.r, ok, el);
+}
+
+// ------------------------------------------------------------------ scans ---
+// Reduce: agg[c] = x[cL] ⊗ .. ⊗ x[min(n, (c+1)L) - 1].
+template <int D, class Op>
+__global__ void __launch_bounds__(kThreads) k_scan_reduce(typename Op::Arr x, int64_t n, int L,
+                                                          typename Op::Arr agg, DevError* err) {
+  extern __shared__ double smem[];
+  const Grp<D> g = make_group<D>(smem);
+  const int64_t c = group_index<D>(g);
+  const int64_t lo = c * L;
+  const int64_t hi = min(n, lo + L);
+  const bool okc = g.real() && lo < n;
+  auto acc = Op::load(x, lo, g.r, okc);
+  bool bad = false;
+  for (int t = 1; t < L; ++t) {
+    const int64_t k = lo + t;
+    const bool ok = okc && k < hi;
+    const auto e = Op::load(x, k, g.r, ok);
+    typename Op::El tmp;
+    const bool good = Op::combine(g, acc, e, tmp);
+    bad |= ok && !good;
+    acc = Op::select(ok, tmp, acc);
+  }
+  if (okc && g.r == 0 && bad) raise_error(err, lo, kErrSingular);
+  Op::store(agg, c, g.r, okc, acc);
+}
+
+// Downsweep: out[k] = carry ⊗ x[lo] ⊗ .. ⊗ x[k] (forward) or
+// x[k] ⊗ .. ⊗ x[hi-1] ⊗ carry (reverse); carry from the scanned aggregates.
+template <int D, class Op, bool kReverse>
+__global__ void __launch_bounds__(kThreads) k_scan_down(typename Op::Arr x, int64_t n, int L,
+                                                        typename Op::Arr aggs, int64_t nchunks,
+                                                        typename Op::Arr out, DevError* err) {
+  extern __shared__ double smem[];
+  const Grp<D> g = make_group<D>(smem);
+  const int64_t c = group_index<D>(g);
+  const int64_t lo = c * L;
+  const int64_t hi = min(n, lo + L);
+  const bool okc = g.real() && lo < n;
+  const int64_t carry_idx = kReverse ? c + 1 : c - 1;
+  bool have = okc && carry_idx >= 0 && carry_idx < nchunks;
+  auto acc = Op::load(aggs, carry_idx, g.r, have);
+  bool bad = false;
+  for (int t = 0; t < L; ++t) {
+    const int64_t k = kReverse ? lo + (L - 1 - t) : lo + t;
+    const bool ok = okc && k < hi;
+    const auto e = Op::load(x, k, g.r, ok);
+    typename Op::El tmp;
+    const bool good = kReverse ? Op::combine(g, e, acc, tmp) : Op::combine(g, acc, e, tmp);
+    bad |= ok && have && !good;
+    acc = Op::select(ok, Op::select(have, tmp, e), acc);
+    have = have || ok;
+    Op::store(out, k, g.r, ok, acc);
+  }
+  if (okc && g.r == 0 && bad) raise_error(err, lo, kErrSingular);
+}
+
+// ------------------------------------------------------------- engine ---
+template <int D>
+struct Engine {
+  static int chunk_len(pode_context* ctx, int64_t n, int level) {
+    const int64_t target = int64_t(ctx->sm_count) * 16 * Grp<D>::kPerWarp;
+    int64_t L = (n + target - 1) / target;
+    const int lmin = level == 0 ? 4 : 8;
+    L = std::max<int64_t>(L, lmin);
+    return static_cast<int>(std::min<int64_t>(L, 256));
+  }
+
+  template <class Op>
+  static typename Op::Arr alloc(pode_context* ctx, const std::string& tag, int64_t n);
+
+  template <class Op, bool kReverse>
+  static void scan_rec(pode_context* ctx, typename Op::Arr in, typename Op::Arr out, int64_t n, int level,
+                       ScanTally& t) {
+    const int L = chunk_len(ctx, n, level);
+    DevError* err = reinterpret_cast<DevError*>(ctx->d_err);
+    if (n <= L) {
+      k_scan_down<D, Op, kReverse><<<1, kThreads, smem_bytes<D>(), ctx->stream>>>(in, n, static_cast<int>(n),
+                                                                                   in, 0, out, err);
+      note_launch(ctx, "scan_down");
+      t.combines += n - 1;
+      t.depth += n - 1;
+      return;
+    }
+    const int64_t nc = (n + L - 1) / L;
+    typename Op::Arr agg = alloc<Op>(ctx, "scan_agg_" + std::to_string(level), nc);
+    k_scan_reduce<D, Op><<<blocks_for<D>(nc), kThreads, smem_bytes<D>(), ctx->stream>>>(in, n, L, agg, err);
+    note_launch(ctx, "scan_reduce");
+    t.combines += n - nc;
+    t.depth += L - 1;
+    scan_rec<Op, kReverse>(ctx, agg, agg, nc, level + 1, t);
+    k_scan_down<D, Op, kReverse><<<blocks_for<D>(nc), kThreads, smem_bytes<D>(), ctx->stream>>>(in, n, L, agg,
+                                                                                                nc, out, err);
+    note_launch(ctx, "scan_down");
+    t.combines += n - 1;
+    t.depth += L;
+  }
+
+  static void set_smem() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    const int bytes = static_cast<int>(smem_bytes<D>());
+    cudaFuncSetAttribute(k_combine<D, FOps<D>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_combine<D, SOps<D>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_make_filtering<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_make_smoothing<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_scan_reduce<D, FOps<D>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_scan_reduce<D, SOps<D>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_scan_down<D, FOps<D>, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_scan_down<D, FOps<D>, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_scan_down<D, SOps<D>, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_scan_down<D, SOps<D>, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  }
+
+  static void combine_filtering(pode_context* ctx, int64_t count, FEd l, FEd r, FEd o) {
+    set_smem();
+    k_combine<D, FOps<D>><<<blocks_for<D>(count), kThreads, smem_bytes<D>(), ctx->stream>>>(
+        count, l, r, o, reinterpret_cast<DevError*>(ctx->d_err));
+    note_launch(ctx, "combine_filtering");
+  }
+  static void combine_smoothing(pode_context* ctx, int64_t count, SEd l, SEd r, SEd o) {
+    set_smem();
+    k_combine<D, SOps<D>><<<blocks_for<D>(count), kThreads, smem_bytes<D>(), ctx->stream>>>(
+        count, l, r, o, reinterpret_cast<DevError*>(ctx->d_err));
+    note_launch(ctx, "combine_smoothing");
+  }
+  static void make_filtering(pode_context* ctx, const DevChain& ch, int absorb, FEd out) {
+    set_smem();
+    k_make_filtering<D><<<blocks_for<D>(ch.N), kThreads, smem_bytes<D>(), ctx->stream>>>(
+        ch, absorb, out, reinterpret_cast<DevError*>(ctx->d_err));
+    note_launch(ctx, "make_filtering");
+  }
+  static void make_smoothing(pode_context* ctx, const DevChain& ch, const double* fm, const double* fc,
+                             SEd out) {
+    set_smem();
+    k_make_smoothing<D><<<blocks_for<D>(ch.N + 1), kThreads, smem_bytes<D>(), ctx->stream>>>(
+        ch, fm, fc, out, reinterpret_cast<DevError*>(ctx->d_err));
+    note_launch(ctx, "make_smoothing");
+  }
+  static ScanTally scan_filtering(pode_context* ctx, int64_t n, FEd in, FEd out, bool reverse) {
+    set_smem();
+    ScanTally t;
+    if (n < 1) return t;
+    if (reverse)
+      scan_rec<FOps<D>, true>(ctx, in, out, n, 0, t);
+    else
+      scan_rec<FOps<D>, false>(ctx, in, out, n, 0, t);
+    return t;
+  }
+  static ScanTally scan_smoothing(pode_context* ctx, int64_t n, SEd in, SEd out, bool reverse) {
+    set_smem();
+    ScanTally t;
+    if (n < 1) return t;
+    if (reverse)
+      scan_rec<SOps<D>, true>(ctx, in, out, n, 0, t);
+    else
+      scan_rec<SOps<D>, false>(ctx, in, out, n, 0, t);
+    return t;
+  }
+
+  // para_rts (parallel.cpp:166-209) on device buffers.
+  static ScanTally rts(pode_context* ctx, const DevChain& ch, double* fmean, double* fcov, double* smean,
+                       double* scov) {
+    const int64_t N = ch.N;
+    FEd fe = alloc<FOps<D>>(ctx, "rts_fe", N);
+    make_filtering(ctx, ch, 1, fe);
+    ScanTally tf = scan_filtering(ctx, N, fe, fe, false);
+    // filtered[0] = init, filtered[n+1] = (b_n, C_n)
+    cuda_check(cudaMemcpyAsync(fmean, ch.init_mean, sizeof(double) * D, cudaMemcpyDeviceToDevice, ctx->stream),
+               "copy init");
+    cuda_check(cudaMemcpyAsync(fcov, ch.init_cov, sizeof(double) * D * D, cudaMemcpyDeviceToDevice, ctx->stream),
+               "copy init");
+    cuda_check(cudaMemcpyAsync(fmean + D, fe.b, sizeof(double) * D * N, cudaMemcpyDeviceToDevice, ctx->stream),
+               "copy filtered");
+    cuda_check(cudaMemcpyAsync(fcov + D * D, fe.c, sizeof(double) * D * D * N, cudaMemcpyDeviceToDevice,
+                               ctx->stream),
+               "copy filtered");
+    SEd se = alloc<SOps<D>>(ctx, "rts_se", N + 1);
+    make_smoothing(ctx, ch, fmean, fcov, se);
+    ScanTally ts = scan_smoothing(ctx, N + 1, se, se, true);
+    if (smean)
+      cuda_check(cudaMemcpyAsync(smean, se.g, sizeof(double) * D * (N + 1), cudaMemcpyDeviceToDevice,
+                                 ctx->stream),
+                 "copy smoothed");
+    if (scov)
+      cuda_check(cudaMemcpyAsync(scov, se.l, sizeof(double) * D * D * (N + 1), cudaMemcpyDeviceToDevice,
+                                 ctx->stream),
+                 "copy smoothed");
+    ScanTally out;
+    out.combines = std::max(tf.combines, ts.combines);
+    out.depth = std::max(tf.depth, ts.depth);
+    return out;
+  }
+};
+
+template <int D>
+template <class Op>
+typename Op::Arr Engine<D>::alloc(pode_context* ctx, const std::string& tag, int64_t n) {
+  if constexpr (std::is_same_v<Op, FOps<D>>) {
+    FEd e;
+    double* base = ctx->ws.arr<double>(tag, size_t(n) * (3 * D * D + 2 * D));
+    e.a = base;
+    e.c = e.a + n * D * D;
+    e.j = e.c + n * D * D;
+    e.b = e.j + n * D * D;
+    e.eta = e.b + n * D;
+    return e;
+  } else {
+    SEd e;
+    double* base = ctx->ws.arr<double>(tag, size_t(n) * (2 * D * D + D));
+    e.e = base;
+    e.l = e.e + n * D * D;
+    e.g = e.l + n * D * D;
+    return e;
+  }
+}
+
+}  // namespace pode

@@ -1,0 +1,432 @@
+// The IEKS Gauss-Newton loop on the device (replaces ieks_drive,
+// proj/src/ieks.cpp:114-210): per-step linearisation, the scan-based
+// smoother, the objective / stopping reductions and the final calibration
+// and projection.  Only the three convergence scalars cross to the host per
+// iteration.
+#pragma once
+
+#include <cmath>
+#include <vector>
+
+#include "engine.cuh"
+#include "host_model.hpp"
+#include "problems.cuh"
+
+namespace pode {
+
+constexpr int kRedThreads = 256;
+
+// Node scales T(h_n) (prior.cpp:79-97) with the incoming step; node 0 uses
+// step 0 (ieks.cpp:28-33).
+static __global__ void k_node_scales(const double* grid, int64_t n1, int nu, int dim, double* scale,
+                              double* scale_inv) {
+  const int64_t n = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (n >= n1) return;
+  const double h = (n == 0) ? grid[1] - grid[0] : grid[n] - grid[n - 1];
+  const double root_h = sqrt(h);
+  const int b = nu + 1, D = b * dim;
+  double fact = 1.0;
+  double taus[8];
+  for (int i = nu; i >= 0; --i) {  // factorial(nu - i) built up as i decreases
+    const int k = nu - i;
+    if (k > 0) fact *= k;
+    taus[i] = root_h * pow(h, double(k)) / fact;
+  }
+  for (int r = 0; r < dim; ++r)
+    for (int i = 0; i <= nu; ++i) {
+      scale[n * D + r * b + i] = taus[i];
+      scale_inv[n * D + r * b + i] = 1.0 / taus[i];
+    }
+}
+
+// Rescaled transitions phi_n = phi_bar diag(T_n ⊙ T_{n+1}^-1) (ieks.cpp:37-45).
+static __global__ void k_transitions(const double* phibar, const double* scale, const double* scale_inv, int64_t N,
+                              int D, double* phi) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t >= N * D) return;
+  const int64_t n = t / D;
+  const int r = int(t - n * D);
+  for (int c = 0; c < D; ++c)
+    phi[(n * D + r) * D + c] = phibar[r * D + c] * (scale[n * D + c] * scale_inv[(n + 1) * D + c]);
+}
+
+static __global__ void k_fill_rows(const double* row, int64_t n, int D, double* out) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t >= n * D) return;
+  out[t] = row[t % D];
+}
+
+// EK1 / EK0 linearisation at eta[i+1], rescaled into node-(i+1) coordinates
+// (statespace.cpp:65-103, ieks.cpp:160-164).  obs rows = d, R = 0.
+template <int DMAX>
+static __global__ void k_linearize(DevProblem prob, int nu, const double* eta, const double* grid,
+                            const double* scale, int64_t N, int ek0, double* h, double* off,
+                            DevError* err) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= N) return;
+  const int d = prob.dim, b = nu + 1, D = d * b;
+  const double* e = eta + (i + 1) * D;
+  const double* s = scale + (i + 1) * D;
+  double y[DMAX], f[DMAX], jac[DMAX * DMAX];
+  for (int r = 0; r < d; ++r) y[r] = e[r * b];
+  eval_field<DMAX>(prob, y, f, jac);
+  bool finite = true;
+  for (int r = 0; r < d; ++r) finite &= isfinite(f[r]);
+  if (!ek0)
+    for (int k = 0; k < d * d; ++k) finite &= isfinite(jac[k]);
+  if (!finite) raise_error(err, i + 1, kErrLinearization);
+  for (int r = 0; r < d; ++r) {
+    double* hr = h + (i * d + r) * D;
+    for (int c = 0; c < D; ++c) hr[c] = 0.0;
+    hr[r * b + 1] = 1.0 * s[r * b + 1];
+    if (ek0) {
+      off[i * d + r] = f[r];
+    } else {
+      double jy = 0.0;
+      for (int c = 0; c < d; ++c) {
+        hr[c * b] = -jac[r * d + c] * s[c * b];
+        jy += jac[r * d + c] * y[c];
+      }
+      off[i * d + r] = f[r] - jy;
+    }
+  }
+}
+
+// new_eta = T ⊙ m_s, plus per-node / per-step terms of the objective
+// (ieks.cpp:49-60, 136-144) and the stopping maxima (ieks.cpp:62-77);
+// one block-level partial per block, summed in a fixed order.
+// smean == nullptr evaluates the objective of eta_old itself (the constant
+// start, ieks.cpp:147-148).
+static __global__ void k_eta_objective(const double* smean, const double* scale, const double* scale_inv,
+                                const double* eta_old, const double* phi, const double* qunit,
+                                const double* qinv_diag, int64_t n1, int D, double* eta_new, double* part) {
+  __shared__ double s_obj[kRedThreads], s_dmax[kRedThreads], s_emax[kRedThreads];
+  const int64_t n = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  auto state = [&](int64_t node, int k) {
+    return smean ? scale[node * D + k] * smean[node * D + k] : eta_old[node * D + k];
+  };
+  double obj = 0.0, dmax = 0.0, emax = 0.0;
+  if (n < n1) {
+    for (int k = 0; k < D; ++k) {
+      const double v = state(n, k);
+      if (smean) eta_new[n * D + k] = v;
+      dmax = fmax(dmax, fabs(v - eta_old[n * D + k]));
+      emax = fmax(emax, fabs(v));
+    }
+  }
+  if (n < n1 - 1) {
+    // increment of step n in rescaled coordinates, whitened by Q_unit^1/2
+    double inc[32], w[32];
+    for (int k = 0; k < D; ++k) {
+      double acc = 0.0;
+      for (int c = 0; c < D; ++c) acc += phi[(n * D + k) * D + c] * (scale_inv[n * D + c] * state(n, c));
+      inc[k] = scale_inv[(n + 1) * D + k] * state(n + 1, k) - acc;
+    }
+    double acc2 = 0.0;
+    for (int k = 0; k < D; ++k) {
+      double a = inc[k];
+      for (int c = 0; c < k; ++c) a -= qunit[k * D + c] * w[c];
+      w[k] = a * qinv_diag[k];
+      acc2 += w[k] * w[k];
+    }
+    obj = acc2;
+  }
+  s_obj[threadIdx.x] = obj;
+  s_dmax[threadIdx.x] = dmax;
+  s_emax[threadIdx.x] = emax;
+  __syncthreads();
+  for (int s = kRedThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      s_obj[threadIdx.x] += s_obj[threadIdx.x + s];
+      s_dmax[threadIdx.x] = fmax(s_dmax[threadIdx.x], s_dmax[threadIdx.x + s]);
+      s_emax[threadIdx.x] = fmax(s_emax[threadIdx.x], s_emax[threadIdx.x + s]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[blockIdx.x * 3 + 0] = s_obj[0];
+    part[blockIdx.x * 3 + 1] = s_dmax[0];
+    part[blockIdx.x * 3 + 2] = s_emax[0];
+  }
+}
+
+// Fixed-order finish of block partials: out = (sum_0, max_1, max_2).
+static __global__ void k_finish3(const double* part, int64_t nparts, double* out) {
+  __shared__ double s0[kRedThreads], s1[kRedThreads], s2[kRedThreads];
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (int64_t k = threadIdx.x; k < nparts; k += blockDim.x) {
+    a += part[k * 3 + 0];
+    b = fmax(b, part[k * 3 + 1]);
+    c = fmax(c, part[k * 3 + 2]);
+  }
+  s0[threadIdx.x] = a;
+  s1[threadIdx.x] = b;
+  s2[threadIdx.x] = c;
+  __syncthreads();
+  for (int s = kRedThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      s0[threadIdx.x] += s0[threadIdx.x + s];
+      s1[threadIdx.x] = fmax(s1[threadIdx.x], s1[threadIdx.x + s]);
+      s2[threadIdx.x] = fmax(s2[threadIdx.x], s2[threadIdx.x + s]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = s0[0];
+    out[1] = s1[0];
+    out[2] = s2[0];
+  }
+}
+
+// Whitened innovation of step i from filtered[i] (innovation_stats,
+// ieks.cpp:79-104): pred = kf_predict(filtered[i]); S = tria([H P^1/2, R^1/2]);
+// value = ||S^-1 (H m - offset)||^2.
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_innovation(DevChain ch, const double* fm, const double* fc,
+                                                         double* values, DevError* err) {
+  extern __shared__ double smem[];
+  const Grp<D> g = make_group<D>(smem);
+  const int64_t i = group_index<D>(g);
+  const bool ok = g.real() && i < ch.N;
+  Gauss<D> f;
+  f.m = ld_ent<D>(fm, i, g.r, ok);
+  f.c = ld_row<D>(fc, i, g.r, ok);
+  const Rw<D> phi = chain_phi<D>(ch, i, g.r, ok);
+  const Rw<D> q = chain_q<D>(ch, i, g.r, ok);
+  const Obs<D, D> o = load_obs<D>(ch, i, g.r, ok);
+  const Gauss<D> p = kf_predict(g, f, phi, q);
+  constexpr int K = 2 * D;
+  Rw<K> top, none = zeros<K>();
+  const Rw<D> hp = mm(g, o.h, p.c);
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    top[j] = hp[j];
+    top[D + j] = o.r[j];
+  }
+  lq<D, D, 0, K>(g, top, none);
+  const bool sing = singular_diag(g, pick(top, g.r), o.m);
+  const double z = matvec(g, o.h, p.m) - o.off;
+  Rw<D> srow;
+#pragma unroll
+  for (int j = 0; j < D; ++j) srow[j] = top[j];
+  publish_factor<D, D>(g, srow);
+  const Rw<D> zv = gather_vec(g, z);
+  const Rw<D> w = solve_vec_lower_all(g, zv);
+  double v = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) v = fma(w[k], w[k], v);
+  if (ok && g.r == 0) {
+    values[i] = v;
+    if (sing) raise_error(err, i, kErrSingular);
+  }
+}
+
+// Fixed-order sum of values[0..n).
+static __global__ void k_sum_blocks(const double* values, int64_t n, double* part) {
+  __shared__ double s[kRedThreads];
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  s[threadIdx.x] = i < n ? values[i] : 0.0;
+  __syncthreads();
+  for (int k = kRedThreads / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) s[threadIdx.x] += s[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[blockIdx.x * 3 + 0] = s[0];
+    part[blockIdx.x * 3 + 1] = 0.0;
+    part[blockIdx.x * 3 + 2] = 0.0;
+  }
+}
+
+// Calibrated outputs in original coordinates (ieks.cpp:196-208).
+static __global__ void k_outputs(const double* eta, const double* scov, const double* scale, double sigma_rel,
+                          int64_t n1, int D, int nu, int dim, double* means, double* cov, double* sol_m,
+                          double* sol_c) {
+  const int64_t n = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (n >= n1) return;
+  const int b = nu + 1;
+  if (means)
+    for (int k = 0; k < D; ++k) means[n * D + k] = eta[n * D + k];
+  if (cov)
+    for (int r = 0; r < D; ++r)
+      for (int c = 0; c < D; ++c) cov[(n * D + r) * D + c] = scale[n * D + r] * scov[(n * D + r) * D + c] * sigma_rel;
+  if (sol_m)
+    for (int r = 0; r < dim; ++r) sol_m[n * dim + r] = eta[n * D + r * b];
+  if (sol_c)
+    for (int r = 0; r < dim; ++r)
+      for (int c = 0; c < dim; ++c) {
+        double acc = 0.0;
+        for (int k = 0; k < D; ++k)
+          acc += (scale[n * D + r * b] * scov[(n * D + r * b) * D + k] * sigma_rel) *
+                 (scale[n * D + c * b] * scov[(n * D + c * b) * D + k] * sigma_rel);
+        sol_c[(n * dim + r) * dim + c] = acc;
+      }
+}
+
+struct IeksResult {
+  int iterations = 0;
+  bool converged = false;
+  double sigma_hat = 0.0;
+  std::vector<double> trace;
+  ScanTally stats;
+};
+
+inline unsigned grid1(int64_t n, int threads = kRedThreads) {
+  return static_cast<unsigned>((n + threads - 1) / threads);
+}
+
+template <int D>
+struct IeksEngine {
+  // v1 driver: linearize -> rts (element kernels + chunked scans) -> reductions.
+  static IeksResult run(pode_context* ctx, const host::Problem& p, const pode_prior& prior,
+                        const double* grid_h, int64_t n1, const pode_ieks_config& cfg, double* means,
+                        double* cov, double* sol_m, double* sol_c) {
+    const int nu = prior.nu, dim = prior.dim;
+    const int64_t N = n1 - 1;
+    cudaStream_t st = ctx->stream;
+    DevError* err = reinterpret_cast<DevError*>(ctx->d_err);
+    Workspace& ws = ctx->ws;
+    double* d_grid = ws.arr<double>("ieks_grid", n1);
+    cuda_check(cudaMemcpyAsync(d_grid, grid_h, sizeof(double) * n1, cudaMemcpyHostToDevice, st), "grid");
+    double* scale = ws.arr<double>("ieks_scale", n1 * D);
+    double* scale_inv = ws.arr<double>("ieks_scale_inv", n1 * D);
+    k_node_scales<<<grid1(n1), kRedThreads, 0, st>>>(d_grid, n1, nu, dim, scale, scale_inv);
+    note_launch(ctx, "node_scales");
+    // constant prior blocks
+    const std::vector<double> phibar = host::preconditioned_phi(nu, dim);
+    const std::vector<double> qunit = host::preconditioned_q_sqrt(nu, dim);
+    std::vector<double> qs(qunit), qinv(D);
+    for (auto& x : qs) x *= prior.sigma;
+    for (int k = 0; k < D; ++k) qinv[k] = 1.0 / qunit[k * D + k];
+    double* d_consts = ws.arr<double>("ieks_consts", 3 * D * D + D + D);
+    double* d_phibar = d_consts;
+    double* d_qunit = d_phibar + D * D;
+    double* d_q = d_qunit + D * D;
+    double* d_qinv = d_q + D * D;
+    double* d_mu0 = d_qinv + D;
+    const std::vector<double> mu0 = host::taylor_init(p, nu);
+    std::vector<double> hc(3 * D * D + 2 * D);
+    std::copy(phibar.begin(), phibar.end(), hc.begin());
+    std::copy(qunit.begin(), qunit.end(), hc.begin() + D * D);
+    std::copy(qs.begin(), qs.end(), hc.begin() + 2 * D * D);
+    std::copy(qinv.begin(), qinv.end(), hc.begin() + 3 * D * D);
+    std::copy(mu0.begin(), mu0.end(), hc.begin() + 3 * D * D + D);
+    cuda_check(cudaMemcpyAsync(d_consts, hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice, st),
+               "consts");
+    double* phi = ws.arr<double>("ieks_phi", N * D * D);
+    k_transitions<<<grid1(N * D), kRedThreads, 0, st>>>(d_phibar, scale, scale_inv, N, D, phi);
+    note_launch(ctx, "transitions");
+    // init_scaled = T_0^-1 ⊙ mu0, zero covariance
+    double* init_m = ws.arr<double>("ieks_init", D + D * D);
+    double* init_c = init_m + D;
+    std::vector<double> si0(D);
+    cuda_check(cudaMemcpyAsync(si0.data(), scale_inv, sizeof(double) * D, cudaMemcpyDeviceToHost, st), "si0");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    std::vector<double> ih(D + D * D, 0.0);
+    for (int k = 0; k < D; ++k) ih[k] = si0[k] * mu0[k];
+    cuda_check(cudaMemcpyAsync(init_m, ih.data(), sizeof(double) * ih.size(), cudaMemcpyHostToDevice, st),
+               "init");
+    // observation buffers (d rows per step, R = 0)
+    double* oh = ws.arr<double>("ieks_h", N * dim * D);
+    double* ooff = ws.arr<double>("ieks_off", N * dim);
+    double* orr = ws.arr<double>("ieks_r", N * dim * dim);
+    int32_t* orows = ws.arr<int32_t>("ieks_rows", N);
+    cuda_check(cudaMemsetAsync(orr, 0, sizeof(double) * N * dim * dim, st), "r");
+    {
+      std::vector<int32_t> rows(N, dim);
+      cuda_check(cudaMemcpyAsync(orows, rows.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, st), "rows");
+      cuda_check(cudaStreamSynchronize(st), "sync");
+    }
+    DevChain ch{D, dim, N, init_m, init_c, phi, d_q, 0, 1, orows, oh, ooff, orr};
+    DevProblem dp{};
+    dp.kind = p.kind;
+    dp.dim = dim;
+    if (p.params.size() > size_t(kMaxParams)) throw ApiError(PODE_ERR_UNSUPPORTED, "too many problem params");
+    for (size_t k = 0; k < p.params.size(); ++k) dp.params[k] = p.params[k];
+
+    double* eta_a = ws.arr<double>("ieks_eta_a", n1 * D);
+    double* eta_b = ws.arr<double>("ieks_eta_b", n1 * D);
+    double* fm = ws.arr<double>("ieks_fm", n1 * D);
+    double* fc = ws.arr<double>("ieks_fc", n1 * D * D);
+    double* sm = ws.arr<double>("ieks_sm", n1 * D);
+    double* sc = ws.arr<double>("ieks_sc", n1 * D * D);
+    const int64_t nparts = grid1(n1);
+    double* part = ws.arr<double>("ieks_part", nparts * 3 + 3);
+    double* red = part + nparts * 3;
+    k_fill_rows<<<grid1(n1 * D), kRedThreads, 0, st>>>(d_mu0, n1, D, eta_a);
+    note_launch(ctx, "fill");
+    auto reduce3 = [&](const double* smean, const double* eold, double* enew) {
+      k_eta_objective<<<grid1(n1), kRedThreads, 0, st>>>(smean, scale, scale_inv, eold, phi, d_qunit, d_qinv,
+                                                         n1, D, enew, part);
+      note_launch(ctx, "eta_objective");
+      k_finish3<<<1, kRedThreads, 0, st>>>(part, nparts, red);
+      note_launch(ctx, "finish3");
+      cuda_check(cudaMemcpyAsync(ctx->h_scalars, red, sizeof(double) * 3, cudaMemcpyDeviceToHost, st), "red");
+      cuda_check(cudaStreamSynchronize(st), "sync");
+    };
+    reduce3(nullptr, eta_a, eta_b);  // objective of the constant start
+    double v_prev = 0.5 * ctx->h_scalars[0];
+    IeksResult res;
+    int it = 0;
+    while (it < cfg.max_iterations) {
+      ++it;
+      reset_error(ctx);
+      k_linearize<D><<<grid1(N), kRedThreads, 0, st>>>(dp, nu, eta_a, d_grid, scale, N, cfg.linearization, oh,
+                                                       ooff, err);
+      note_launch(ctx, "linearize");
+      const unsigned long long key = fetch_error(ctx);
+      if (key != ~0ull) {
+        const int64_t idx = int64_t(key >> 8);
+        double t = 0.0;
+        cuda_check(cudaMemcpy(&t, d_grid + idx, sizeof(double), cudaMemcpyDeviceToHost), "t");
+        throw ApiError(PODE_ERR_LINEARIZATION,
+                       "ieks iteration " + std::to_string(it) +
+                           ": linearize: vector field evaluation is not finite",
+                       idx, t, it);
+      }
+      const ScanTally t = Engine<D>::rts(ctx, ch, fm, fc, sm, sc);
+      res.stats.combines = std::max(res.stats.combines, t.combines);
+      res.stats.depth = std::max(res.stats.depth, t.depth);
+      reduce3(sm, eta_a, eta_b);
+      const unsigned long long key2 = fetch_error(ctx);
+      if (key2 != ~0ull)
+        throw ApiError(PODE_ERR_SINGULAR_FACTOR, "ieks iteration " + std::to_string(it) +
+                                                     ": smoother: triangular factor is singular",
+                       int64_t(key2 >> 8), 0.0, it);
+      const double v = 0.5 * ctx->h_scalars[0];
+      const double dmax = ctx->h_scalars[1], emax = ctx->h_scalars[2];
+      res.trace.push_back(v);
+      const bool conv = (dmax <= cfg.traj_rtol * emax) ||
+                        (std::fabs(v - v_prev) <= cfg.obj_atol + cfg.obj_rtol * std::fabs(v));
+      std::swap(eta_a, eta_b);
+      v_prev = v;
+      if (conv) {
+        res.converged = true;
+        break;
+      }
+    }
+    res.iterations = it;
+    // calibration from the final pass' innovations
+    double* vals = ws.arr<double>("ieks_innov", N);
+    k_innovation<D><<<blocks_for<D>(N), kThreads, smem_bytes<D>(), st>>>(ch, fm, fc, vals, err);
+    note_launch(ctx, "innovation");
+    const int64_t np2 = grid1(N);
+    double* part2 = ws.arr<double>("ieks_part2", np2 * 3 + 3);
+    k_sum_blocks<<<np2, kRedThreads, 0, st>>>(vals, N, part2);
+    note_launch(ctx, "sum_blocks");
+    k_finish3<<<1, kRedThreads, 0, st>>>(part2, np2, part2 + np2 * 3);
+    note_launch(ctx, "finish3");
+    double sq = 0.0;
+    cuda_check(cudaMemcpyAsync(&sq, part2 + np2 * 3, sizeof(double), cudaMemcpyDeviceToHost, st), "innov");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    const int64_t count = N * dim;
+    const double sigma_rel = std::sqrt(sq / double(count));
+    res.sigma_hat = sigma_rel * prior.sigma;
+    k_outputs<<<grid1(n1), kRedThreads, 0, st>>>(eta_a, sc, scale, sigma_rel, n1, D, nu, dim, means, cov, sol_m,
+                                                 sol_c);
+    note_launch(ctx, "outputs");
+    return res;
+  }
+};
+
+}  // namespace pode

@@ -1,0 +1,43 @@
+// Instantiates the engine for one state dimension; included by inst_dN.cu
+// with PODE_D defined, so the per-D kernels compile in parallel.
+#include "dispatch.hpp"
+#include "ieks.cuh"
+
+#ifndef PODE_D
+#error "define PODE_D"
+#endif
+
+namespace pode {
+
+#define PODE_CAT2(a, b) a##b
+#define PODE_CAT(a, b) PODE_CAT2(a, b)
+
+namespace {
+constexpr int kD = PODE_D;
+using E = Engine<kD>;
+
+void cf(pode_context* c, int64_t n, const FEd& l, const FEd& r, const FEd& o) { E::combine_filtering(c, n, l, r, o); }
+void cs(pode_context* c, int64_t n, const SEd& l, const SEd& r, const SEd& o) { E::combine_smoothing(c, n, l, r, o); }
+void mf(pode_context* c, const DevChain& ch, int a, const FEd& o) { E::make_filtering(c, ch, a, o); }
+void ms(pode_context* c, const DevChain& ch, const double* fm, const double* fc, const SEd& o) {
+  E::make_smoothing(c, ch, fm, fc, o);
+}
+void sf(pode_context* c, int64_t n, const FEd& i, const FEd& o, bool rev, ScanTally* t) {
+  *t = E::scan_filtering(c, n, i, o, rev);
+}
+void ss(pode_context* c, int64_t n, const SEd& i, const SEd& o, bool rev, ScanTally* t) {
+  *t = E::scan_smoothing(c, n, i, o, rev);
+}
+void rt(pode_context* c, const DevChain& ch, double* fm, double* fc, double* sm, double* sc, ScanTally* t) {
+  *t = E::rts(c, ch, fm, fc, sm, sc);
+}
+void ik(pode_context* c, const host::Problem& p, const pode_prior& pr, const double* g, int64_t n1,
+        const pode_ieks_config& cfg, double* m, double* cv, double* sm, double* sc, IeksResult* out) {
+  *out = IeksEngine<kD>::run(c, p, pr, g, n1, cfg, m, cv, sm, sc);
+}
+const EngineOps kOps{kD, cf, cs, mf, ms, sf, ss, rt, ik};
+}  // namespace
+
+const EngineOps* PODE_CAT(engine_ops_d, PODE_D)() { return &kOps; }
+
+}  // namespace pode
