@@ -164,6 +164,39 @@ struct SOps {
   }
 };
 
+// Mean-only smoothing elements (E, g): the IEKS iterations need smoothed
+// means only; covariances are formed once after convergence.
+template <int D>
+struct MOps {
+  struct El {
+    Rw<D> e;
+    double g;
+  };
+  using Arr = SEd;  // l unused
+  __device__ static El load(const Arr& x, int64_t i, int r, bool ok) {
+    El e;
+    e.e = ld_row<D>(x.e, i, r, ok);
+    e.g = ld_ent<D>(x.g, i, r, ok);
+    return e;
+  }
+  __device__ static void store(const Arr& x, int64_t i, int r, bool ok, const El& e) {
+    st_row<D>(x.e, i, r, ok, e.e);
+    st_ent<D>(x.g, i, r, ok, e.g);
+  }
+  __device__ static bool combine(const Grp<D>& g, const El& l, const El& rr, El& out) {
+    out.e = mm(g, l.e, rr.e);
+    out.g = matvec(g, l.e, rr.g) + l.g;
+    return true;
+  }
+  __device__ static El select(bool take_a, const El& a, const El& b) {
+    El o;
+#pragma unroll
+    for (int j = 0; j < D; ++j) o.e[j] = take_a ? a.e[j] : b.e[j];
+    o.g = take_a ? a.g : b.g;
+    return o;
+  }
+};
+
 // ------------------------------------------------------ batched combines ---
 template <int D, class Op>
 __global__ void __launch_bounds__(kThreads) k_combine(int64_t count, typename Op::Arr lhs,
@@ -320,10 +353,13 @@ __global__ void __launch_bounds__(kThreads) k_scan_down(typename Op::Arr x, int6
 // ------------------------------------------------------------- engine ---
 template <int D>
 struct Engine {
+  // Chunk length per recursion level: level 0 fills the GPU; upper levels are
+  // latency-bound (each group runs L dependent combines), so they use short
+  // chunks and more levels.
   static int chunk_len(pode_context* ctx, int64_t n, int level) {
     const int64_t target = int64_t(ctx->sm_count) * 16 * Grp<D>::kPerWarp;
     int64_t L = (n + target - 1) / target;
-    const int lmin = level == 0 ? 4 : 8;
+    const int lmin = level == 0 ? 4 : 4;
     L = std::max<int64_t>(L, lmin);
     return static_cast<int>(std::min<int64_t>(L, 256));
   }
@@ -373,6 +409,16 @@ struct Engine {
     cudaFuncSetAttribute(k_scan_down<D, FOps<D>, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(k_scan_down<D, SOps<D>, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(k_scan_down<D, SOps<D>, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_scan_reduce<D, MOps<D>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_scan_down<D, MOps<D>, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  }
+
+  // Reverse inclusive scan of mean-only smoothing elements.
+  static ScanTally scan_means_reverse(pode_context* ctx, int64_t n, SEd io) {
+    set_smem();
+    ScanTally t;
+    if (n >= 1) scan_rec<MOps<D>, true>(ctx, io, io, n, 0, t);
+    return t;
   }
 
   static void combine_filtering(pode_context* ctx, int64_t count, FEd l, FEd r, FEd o) {

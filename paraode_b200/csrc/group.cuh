@@ -216,67 +216,142 @@ __device__ __forceinline__ Rw<D> transpose(const Grp<D>& g, const Rw<D>& a) {
 // transpose (beta = -sign(c0) ||x||, essential = tail / (c0 - beta),
 // tau = (beta - c0) / beta; tau = 0 when ||tail||^2 <= DBL_MIN).  On return
 // the rows hold L (lower triangular in pivot order); L L^T = M M^T.
+// Sum of squares of x[lo..K) with four independent accumulators (short
+// dependency chains; every lane evaluates it identically).
+template <int K>
+__device__ __forceinline__ double sumsq_from(const Rw<K>& x, int lo) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+  for (int j = lo; j < K; ++j) {
+    const int s = (j - lo) & 3;
+    if (s == 0) a0 = fma(x[j], x[j], a0);
+    if (s == 1) a1 = fma(x[j], x[j], a1);
+    if (s == 2) a2 = fma(x[j], x[j], a2);
+    if (s == 3) a3 = fma(x[j], x[j], a3);
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
+template <int K>
+__device__ __forceinline__ double dot_from(const Rw<K>& x, const Rw<K>& y, int lo, double init) {
+  double a0 = init, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+  for (int j = lo; j < K; ++j) {
+    const int s = (j - lo) & 3;
+    if (s == 0) a0 = fma(x[j], y[j], a0);
+    if (s == 1) a1 = fma(x[j], y[j], a1);
+    if (s == 2) a2 = fma(x[j], y[j], a2);
+    if (s == 3) a3 = fma(x[j], y[j], a3);
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
+// Householder reflector of x[p..K) in Eigen's convention; every lane of the
+// group computes it redundantly from the shuffled pivot row (no owner-only
+// serial section, no shared-memory round trip).
+template <int K>
+struct Reflector {
+  double tau, beta;
+  Rw<K> ess;  // ess[j], j > p
+};
+
+template <int K>
+__device__ __forceinline__ Reflector<K> make_reflector(const Rw<K>& x, int p) {
+  Reflector<K> h;
+  const double tail = sumsq_from(x, p + 1);
+  const double c0 = x[p];
+  h.tau = 0.0;
+  h.beta = c0;
+  double inv = 0.0;
+  if (tail > DBL_MIN) {
+    double beta = sqrt(fma(c0, c0, tail));
+    beta = (c0 >= 0.0) ? -beta : beta;
+    inv = __drcp_rn(c0 - beta);
+    h.tau = (beta - c0) * __drcp_rn(beta);
+    h.beta = beta;
+  }
+#pragma unroll
+  for (int j = p + 1; j < K; ++j) h.ess[j] = x[j] * inv;
+  return h;
+}
+
+// y <- y (I - tau v v^T), v = [1, ess] on columns p..K-1.
+template <int K>
+__device__ __forceinline__ void apply_reflector(const Reflector<K>& h, int p, Rw<K>& y) {
+  const double w = dot_from(y, h.ess, p + 1, y[p]);
+  const double tw = h.tau * w;
+  y[p] -= tw;
+#pragma unroll
+  for (int j = p + 1; j < K; ++j) y[j] = fma(-tw, h.ess[j], y[j]);
+}
+
+// Row p of a register row set, fetched from its owner lane.
+template <int D, int K>
+__device__ __forceinline__ Rw<K> shfl_row(const Grp<D>& g, const Rw<K>& row, int owner, int from) {
+  const int src = (threadIdx.x & 31) - g.r + owner;
+  Rw<K> x;
+#pragma unroll
+  for (int j = 0; j < K; ++j) x[j] = (j >= from) ? __shfl_sync(0xffffffffu, row[j], src) : 0.0;
+  return x;
+}
+
 template <int D, int NT, int NB, int K>
 __device__ __forceinline__ void lq(const Grp<D>& g, Rw<K>& top, Rw<K>& bot) {
   constexpr int kPivots = (NT + NB < K) ? (NT + NB) : K;
-  double* vb = g.vs + 3 * D;  // reflector: vb[0] = tau, vb[1 + j] = essential_j (j > p)
 #pragma unroll
   for (int p = 0; p < kPivots; ++p) {
     const bool in_top = p < NT;
     const int owner = in_top ? p : p - NT;
-    wsync();
-    if (g.r == owner) {
-      const Rw<K>& row = in_top ? top : bot;
-      double tail = 0.0;
-#pragma unroll
-      for (int j = p + 1; j < K; ++j) tail = fma(row[j], row[j], tail);
-      const double c0 = row[p];
-      double tau = 0.0, beta = c0, inv = 0.0;
-      if (tail > DBL_MIN) {
-        beta = sqrt(fma(c0, c0, tail));
-        if (c0 >= 0.0) beta = -beta;
-        inv = 1.0 / (c0 - beta);
-        tau = (beta - c0) / beta;
-      }
-      vb[0] = tau;
-#pragma unroll
-      for (int j = p + 1; j < K; ++j) vb[1 + j] = row[j] * inv;
-      vb[1] = beta;
-    }
-    wsync();
-    const double tau = vb[0];
-    const double beta = vb[1];
-    Rw<K> ess;
-#pragma unroll
-    for (int j = p + 1; j < K; ++j) ess[j] = vb[1 + j];
+    const Reflector<K> h = make_reflector(shfl_row(g, in_top ? top : bot, owner, p), p);
+    const double tau = h.tau;
+    const double beta = h.beta;
+    const Rw<K>& ess = h.ess;
     // Apply H = I - tau v v^T (v = [1, ess]) from the right to every row but
     // the pivot row; rows already reduced have zeros from column p on, so the
     // update leaves them unchanged.
-    auto apply = [&](Rw<K>& y) {
-      double w = y[p];
-#pragma unroll
-      for (int j = p + 1; j < K; ++j) w = fma(y[j], ess[j], w);
-      const double tw = tau * w;
-      y[p] -= tw;
-#pragma unroll
-      for (int j = p + 1; j < K; ++j) y[j] = fma(-tw, ess[j], y[j]);
-    };
+    (void)tau;
+    (void)ess;
+    // Rows already reduced have zeros from column p on, so applying the
+    // reflector to every row leaves them unchanged; the pivot row itself
+    // becomes [.., beta, 0, ..] (branch-free select, no divergence).
+    const bool own = g.r == owner;
     if (in_top) {
-      if (g.r == owner) {
+      apply_reflector(h, p, top);
+      apply_reflector(h, p, bot);
+      if (own) {
         top[p] = beta;
 #pragma unroll
         for (int j = p + 1; j < K; ++j) top[j] = 0.0;
-      } else {
-        apply(top);
       }
-      apply(bot);
     } else {
-      if (g.r == owner) {
+      apply_reflector(h, p, bot);
+      if (own) {
         bot[p] = beta;
 #pragma unroll
         for (int j = p + 1; j < K; ++j) bot[j] = 0.0;
-      } else {
-        apply(bot);
+      }
+    }
+  }
+}
+
+// Two independent LQs of D x K row sets run in one pivot sweep (their
+// reflectors are independent, so the two dependency chains overlap).
+template <int D, int K>
+__device__ __forceinline__ void lq_pair(const Grp<D>& g, Rw<K>& a, Rw<K>& b) {
+  constexpr int kPivots = (D < K) ? D : K;
+#pragma unroll
+  for (int p = 0; p < kPivots; ++p) {
+    const Reflector<K> ha = make_reflector(shfl_row(g, a, p, p), p);
+    const Reflector<K> hb = make_reflector(shfl_row(g, b, p, p), p);
+    apply_reflector(ha, p, a);
+    apply_reflector(hb, p, b);
+    if (g.r == p) {
+      a[p] = ha.beta;
+      b[p] = hb.beta;
+#pragma unroll
+      for (int j = p + 1; j < K; ++j) {
+        a[j] = 0.0;
+        b[j] = 0.0;
       }
     }
   }

@@ -10,7 +10,7 @@
 
 #include "engine.cuh"
 #include "host_model.hpp"
-#include "problems.cuh"
+#include "field.cuh"
 
 namespace pode {
 
@@ -73,7 +73,8 @@ static __global__ void k_linearize(DevProblem prob, int nu, const double* eta, c
   bool finite = true;
   for (int r = 0; r < d; ++r) finite &= isfinite(f[r]);
   if (!ek0)
-    for (int k = 0; k < d * d; ++k) finite &= isfinite(jac[k]);
+    for (int r = 0; r < d; ++r)
+      for (int c = 0; c < d; ++c) finite &= isfinite(jac[r * DMAX + c]);
   if (!finite) raise_error(err, i + 1, kErrLinearization);
   for (int r = 0; r < d; ++r) {
     double* hr = h + (i * d + r) * D;
@@ -84,8 +85,8 @@ static __global__ void k_linearize(DevProblem prob, int nu, const double* eta, c
     } else {
       double jy = 0.0;
       for (int c = 0; c < d; ++c) {
-        hr[c * b] = -jac[r * d + c] * s[c * b];
-        jy += jac[r * d + c] * y[c];
+        hr[c * b] = -jac[r * DMAX + c] * s[c * b];
+        jy += jac[r * DMAX + c] * y[c];
       }
       off[i * d + r] = f[r] - jy;
     }
@@ -275,75 +276,178 @@ inline unsigned grid1(int64_t n, int threads = kRedThreads) {
   return static_cast<unsigned>((n + threads - 1) / threads);
 }
 
+// Everything a solve needs on the device besides the iteration itself.
+template <int D>
+struct IeksSetup {
+  int nu = 0, dim = 0;
+  int64_t N = 0, n1 = 0;
+  double* grid = nullptr;
+  double* scale = nullptr;
+  double* scale_inv = nullptr;
+  double* phibar = nullptr;
+  double* qunit = nullptr;
+  double* q = nullptr;
+  double* qinv = nullptr;
+  double* mu0 = nullptr;
+  double* init_m = nullptr;  // T_0^-1 mu0, then D*D zeros
+  std::vector<double> h_qunit, h_q, h_qinv, h_m0;
+  DevProblem prob{};
+};
+
 template <int D>
 struct IeksEngine {
-  // v1 driver: linearize -> rts (element kernels + chunked scans) -> reductions.
-  static IeksResult run(pode_context* ctx, const host::Problem& p, const pode_prior& prior,
-                        const double* grid_h, int64_t n1, const pode_ieks_config& cfg, double* means,
-                        double* cov, double* sol_m, double* sol_c) {
-    const int nu = prior.nu, dim = prior.dim;
-    const int64_t N = n1 - 1;
+  static void setup(pode_context* ctx, const host::Problem& p, const pode_prior& prior, const double* grid_h,
+                    int64_t n1, IeksSetup<D>& s) {
+    s.nu = prior.nu;
+    s.dim = prior.dim;
+    s.n1 = n1;
+    s.N = n1 - 1;
     cudaStream_t st = ctx->stream;
-    DevError* err = reinterpret_cast<DevError*>(ctx->d_err);
     Workspace& ws = ctx->ws;
-    double* d_grid = ws.arr<double>("ieks_grid", n1);
-    cuda_check(cudaMemcpyAsync(d_grid, grid_h, sizeof(double) * n1, cudaMemcpyHostToDevice, st), "grid");
-    double* scale = ws.arr<double>("ieks_scale", n1 * D);
-    double* scale_inv = ws.arr<double>("ieks_scale_inv", n1 * D);
-    k_node_scales<<<grid1(n1), kRedThreads, 0, st>>>(d_grid, n1, nu, dim, scale, scale_inv);
+    s.grid = ws.arr<double>("ieks_grid", n1);
+    cuda_check(cudaMemcpyAsync(s.grid, grid_h, sizeof(double) * n1, cudaMemcpyHostToDevice, st), "grid");
+    s.scale = ws.arr<double>("ieks_scale", n1 * D);
+    s.scale_inv = ws.arr<double>("ieks_scale_inv", n1 * D);
+    k_node_scales<<<grid1(n1), kRedThreads, 0, st>>>(s.grid, n1, s.nu, s.dim, s.scale, s.scale_inv);
     note_launch(ctx, "node_scales");
-    // constant prior blocks
-    const std::vector<double> phibar = host::preconditioned_phi(nu, dim);
-    const std::vector<double> qunit = host::preconditioned_q_sqrt(nu, dim);
-    std::vector<double> qs(qunit), qinv(D);
-    for (auto& x : qs) x *= prior.sigma;
-    for (int k = 0; k < D; ++k) qinv[k] = 1.0 / qunit[k * D + k];
-    double* d_consts = ws.arr<double>("ieks_consts", 3 * D * D + D + D);
-    double* d_phibar = d_consts;
-    double* d_qunit = d_phibar + D * D;
-    double* d_q = d_qunit + D * D;
-    double* d_qinv = d_q + D * D;
-    double* d_mu0 = d_qinv + D;
-    const std::vector<double> mu0 = host::taylor_init(p, nu);
+    const std::vector<double> phibar = host::preconditioned_phi(s.nu, s.dim);
+    s.h_qunit = host::preconditioned_q_sqrt(s.nu, s.dim);
+    s.h_q = s.h_qunit;
+    for (auto& x : s.h_q) x *= prior.sigma;
+    s.h_qinv.resize(D);
+    for (int k = 0; k < D; ++k) s.h_qinv[k] = 1.0 / s.h_qunit[k * D + k];
+    double* c = ws.arr<double>("ieks_consts", 3 * D * D + 2 * D + D + D * D);
+    s.phibar = c;
+    s.qunit = c + D * D;
+    s.q = c + 2 * D * D;
+    s.qinv = c + 3 * D * D;
+    s.mu0 = s.qinv + D;
+    s.init_m = s.mu0 + D;
+    const std::vector<double> mu0 = host::taylor_init(p, s.nu);
     std::vector<double> hc(3 * D * D + 2 * D);
     std::copy(phibar.begin(), phibar.end(), hc.begin());
-    std::copy(qunit.begin(), qunit.end(), hc.begin() + D * D);
-    std::copy(qs.begin(), qs.end(), hc.begin() + 2 * D * D);
-    std::copy(qinv.begin(), qinv.end(), hc.begin() + 3 * D * D);
+    std::copy(s.h_qunit.begin(), s.h_qunit.end(), hc.begin() + D * D);
+    std::copy(s.h_q.begin(), s.h_q.end(), hc.begin() + 2 * D * D);
+    std::copy(s.h_qinv.begin(), s.h_qinv.end(), hc.begin() + 3 * D * D);
     std::copy(mu0.begin(), mu0.end(), hc.begin() + 3 * D * D + D);
-    cuda_check(cudaMemcpyAsync(d_consts, hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice, st),
-               "consts");
-    double* phi = ws.arr<double>("ieks_phi", N * D * D);
-    k_transitions<<<grid1(N * D), kRedThreads, 0, st>>>(d_phibar, scale, scale_inv, N, D, phi);
-    note_launch(ctx, "transitions");
-    // init_scaled = T_0^-1 ⊙ mu0, zero covariance
-    double* init_m = ws.arr<double>("ieks_init", D + D * D);
-    double* init_c = init_m + D;
+    cuda_check(cudaMemcpyAsync(c, hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice, st), "consts");
     std::vector<double> si0(D);
-    cuda_check(cudaMemcpyAsync(si0.data(), scale_inv, sizeof(double) * D, cudaMemcpyDeviceToHost, st), "si0");
+    cuda_check(cudaMemcpyAsync(si0.data(), s.scale_inv, sizeof(double) * D, cudaMemcpyDeviceToHost, st), "si0");
     cuda_check(cudaStreamSynchronize(st), "sync");
-    std::vector<double> ih(D + D * D, 0.0);
-    for (int k = 0; k < D; ++k) ih[k] = si0[k] * mu0[k];
-    cuda_check(cudaMemcpyAsync(init_m, ih.data(), sizeof(double) * ih.size(), cudaMemcpyHostToDevice, st),
+    s.h_m0.assign(D + D * D, 0.0);
+    for (int k = 0; k < D; ++k) s.h_m0[k] = si0[k] * mu0[k];
+    cuda_check(cudaMemcpyAsync(s.init_m, s.h_m0.data(), sizeof(double) * s.h_m0.size(), cudaMemcpyHostToDevice, st),
                "init");
-    // observation buffers (d rows per step, R = 0)
+    s.prob.kind = p.kind;
+    s.prob.dim = s.dim;
+    if (p.params.size() > size_t(kMaxParams)) throw ApiError(PODE_ERR_UNSUPPORTED, "too many problem params");
+    for (size_t k = 0; k < p.params.size(); ++k) s.prob.params[k] = p.params[k];
+  }
+
+  // Observation buffers of a DevChain with rescaled transitions (d rows, R = 0).
+  static DevChain chain(pode_context* ctx, const IeksSetup<D>& s, bool materialise_phi) {
+    Workspace& ws = ctx->ws;
+    cudaStream_t st = ctx->stream;
+    const int64_t N = s.N;
+    const int dim = s.dim;
+    double* phi = ws.arr<double>("ieks_phi", N * D * D);
+    if (materialise_phi) {
+      k_transitions<<<grid1(N * D), kRedThreads, 0, st>>>(s.phibar, s.scale, s.scale_inv, N, D, phi);
+      note_launch(ctx, "transitions");
+    }
     double* oh = ws.arr<double>("ieks_h", N * dim * D);
     double* ooff = ws.arr<double>("ieks_off", N * dim);
     double* orr = ws.arr<double>("ieks_r", N * dim * dim);
     int32_t* orows = ws.arr<int32_t>("ieks_rows", N);
     cuda_check(cudaMemsetAsync(orr, 0, sizeof(double) * N * dim * dim, st), "r");
-    {
-      std::vector<int32_t> rows(N, dim);
-      cuda_check(cudaMemcpyAsync(orows, rows.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, st), "rows");
-      cuda_check(cudaStreamSynchronize(st), "sync");
-    }
-    DevChain ch{D, dim, N, init_m, init_c, phi, d_q, 0, 1, orows, oh, ooff, orr};
-    DevProblem dp{};
-    dp.kind = p.kind;
-    dp.dim = dim;
-    if (p.params.size() > size_t(kMaxParams)) throw ApiError(PODE_ERR_UNSUPPORTED, "too many problem params");
-    for (size_t k = 0; k < p.params.size(); ++k) dp.params[k] = p.params[k];
+    std::vector<int32_t> rows(N, dim);
+    cuda_check(cudaMemcpyAsync(orows, rows.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, st), "rows");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    return DevChain{D, dim, N, s.init_m, s.init_m + D, phi, s.q, 0, 1, orows, oh, ooff, orr};
+  }
 
+  static void linearize(pode_context* ctx, const IeksSetup<D>& s, const DevChain& ch, const double* eta, int ek0,
+                        int it) {
+    DevError* err = reinterpret_cast<DevError*>(ctx->d_err);
+    reset_error(ctx);
+    k_linearize<D><<<grid1(s.N), kRedThreads, 0, ctx->stream>>>(s.prob, s.nu, eta, s.grid, s.scale, s.N, ek0,
+                                                                const_cast<double*>(ch.h),
+                                                                const_cast<double*>(ch.off), err);
+    note_launch(ctx, "linearize");
+    check_linearization(ctx, s, it);
+  }
+
+  static void check_linearization(pode_context* ctx, const IeksSetup<D>& s, int it) {
+    const unsigned long long key = fetch_error(ctx);
+    if (key == ~0ull) return;
+    const int code = int(key & 0xff);
+    const int64_t idx = int64_t(key >> 8);
+    if (code == kErrLinearization) {
+      double t = 0.0;
+      cuda_check(cudaMemcpy(&t, s.grid + idx, sizeof(double), cudaMemcpyDeviceToHost), "t");
+      throw ApiError(PODE_ERR_LINEARIZATION,
+                     "ieks iteration " + std::to_string(it) + ": linearize: vector field evaluation is not finite",
+                     idx, t, it);
+    }
+    throw ApiError(PODE_ERR_SINGULAR_FACTOR,
+                   "ieks iteration " + std::to_string(it) + ": smoother: triangular factor is singular", idx, 0.0, it);
+  }
+
+  // After the loop: smoothing covariances and the filtered marginals of the
+  // final linearisation, innovation statistics, calibration and projection
+  // (ieks.cpp:190-208).  `eta_lin` is the final iteration's linearisation
+  // point, `eta_out` its result.
+  static void finalize(pode_context* ctx, const IeksSetup<D>& s, const double* eta_lin, const double* eta_out,
+                       int ek0, int it, double sigma, double* means, double* cov, double* sol_m, double* sol_c,
+                       IeksResult& res) {
+    cudaStream_t st = ctx->stream;
+    Workspace& ws = ctx->ws;
+    DevError* err = reinterpret_cast<DevError*>(ctx->d_err);
+    const int64_t N = s.N, n1 = s.n1;
+    const DevChain ch = chain(ctx, s, true);
+    linearize(ctx, s, ch, eta_lin, ek0, it);
+    double* fm = ws.arr<double>("ieks_fm", n1 * D);
+    double* fc = ws.arr<double>("ieks_fc", n1 * D * D);
+    double* sm = ws.arr<double>("ieks_sm", n1 * D);
+    double* sc = ws.arr<double>("ieks_sc", n1 * D * D);
+    reset_error(ctx);
+    const ScanTally t = Engine<D>::rts(ctx, ch, fm, fc, sm, sc);
+    res.stats.combines = std::max(res.stats.combines, t.combines);
+    res.stats.depth = std::max(res.stats.depth, t.depth);
+    double* vals = ws.arr<double>("ieks_innov", N);
+    cuda_check(cudaFuncSetAttribute(k_innovation<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(smem_bytes<D>())),
+               "innovation smem");
+    k_innovation<D><<<blocks_for<D>(N), kThreads, smem_bytes<D>(), st>>>(ch, fm, fc, vals, err);
+    note_launch(ctx, "innovation");
+    const int64_t np2 = grid1(N);
+    double* part2 = ws.arr<double>("ieks_part2", np2 * 3 + 3);
+    k_sum_blocks<<<np2, kRedThreads, 0, st>>>(vals, N, part2);
+    note_launch(ctx, "sum_blocks");
+    k_finish3<<<1, kRedThreads, 0, st>>>(part2, np2, part2 + np2 * 3);
+    note_launch(ctx, "finish3");
+    cuda_check(cudaMemcpyAsync(ctx->h_scalars, part2 + np2 * 3, sizeof(double), cudaMemcpyDeviceToHost, st),
+               "innov");
+    check_linearization(ctx, s, it);  // syncs
+    const double sq = ctx->h_scalars[0];
+    const int64_t count = N * s.dim;
+    const double sigma_rel = std::sqrt(sq / double(count));
+    res.sigma_hat = sigma_rel * sigma;
+    k_outputs<<<grid1(n1), kRedThreads, 0, st>>>(eta_out, sc, s.scale, sigma_rel, n1, D, s.nu, s.dim, means, cov,
+                                                 sol_m, sol_c);
+    note_launch(ctx, "outputs");
+  }
+
+  // Element/scan driver (any D): linearize -> para_rts -> reductions,
+  // exactly the reference's per-iteration structure.
+  static IeksResult run(pode_context* ctx, const host::Problem& p, const pode_prior& prior, const double* grid_h,
+                        int64_t n1, const pode_ieks_config& cfg, double* means, double* cov, double* sol_m,
+                        double* sol_c) {
+    IeksSetup<D> s;
+    setup(ctx, p, prior, grid_h, n1, s);
+    cudaStream_t st = ctx->stream;
+    Workspace& ws = ctx->ws;
+    const DevChain ch = chain(ctx, s, true);
     double* eta_a = ws.arr<double>("ieks_eta_a", n1 * D);
     double* eta_b = ws.arr<double>("ieks_eta_b", n1 * D);
     double* fm = ws.arr<double>("ieks_fm", n1 * D);
@@ -353,46 +457,29 @@ struct IeksEngine {
     const int64_t nparts = grid1(n1);
     double* part = ws.arr<double>("ieks_part", nparts * 3 + 3);
     double* red = part + nparts * 3;
-    k_fill_rows<<<grid1(n1 * D), kRedThreads, 0, st>>>(d_mu0, n1, D, eta_a);
+    k_fill_rows<<<grid1(n1 * D), kRedThreads, 0, st>>>(s.mu0, n1, D, eta_a);
     note_launch(ctx, "fill");
     auto reduce3 = [&](const double* smean, const double* eold, double* enew) {
-      k_eta_objective<<<grid1(n1), kRedThreads, 0, st>>>(smean, scale, scale_inv, eold, phi, d_qunit, d_qinv,
-                                                         n1, D, enew, part);
+      k_eta_objective<<<grid1(n1), kRedThreads, 0, st>>>(smean, s.scale, s.scale_inv, eold, ch.phi, s.qunit,
+                                                         s.qinv, n1, D, enew, part);
       note_launch(ctx, "eta_objective");
       k_finish3<<<1, kRedThreads, 0, st>>>(part, nparts, red);
       note_launch(ctx, "finish3");
       cuda_check(cudaMemcpyAsync(ctx->h_scalars, red, sizeof(double) * 3, cudaMemcpyDeviceToHost, st), "red");
       cuda_check(cudaStreamSynchronize(st), "sync");
     };
-    reduce3(nullptr, eta_a, eta_b);  // objective of the constant start
+    reduce3(nullptr, eta_a, eta_b);
     double v_prev = 0.5 * ctx->h_scalars[0];
     IeksResult res;
     int it = 0;
     while (it < cfg.max_iterations) {
       ++it;
-      reset_error(ctx);
-      k_linearize<D><<<grid1(N), kRedThreads, 0, st>>>(dp, nu, eta_a, d_grid, scale, N, cfg.linearization, oh,
-                                                       ooff, err);
-      note_launch(ctx, "linearize");
-      const unsigned long long key = fetch_error(ctx);
-      if (key != ~0ull) {
-        const int64_t idx = int64_t(key >> 8);
-        double t = 0.0;
-        cuda_check(cudaMemcpy(&t, d_grid + idx, sizeof(double), cudaMemcpyDeviceToHost), "t");
-        throw ApiError(PODE_ERR_LINEARIZATION,
-                       "ieks iteration " + std::to_string(it) +
-                           ": linearize: vector field evaluation is not finite",
-                       idx, t, it);
-      }
+      linearize(ctx, s, ch, eta_a, cfg.linearization, it);
       const ScanTally t = Engine<D>::rts(ctx, ch, fm, fc, sm, sc);
       res.stats.combines = std::max(res.stats.combines, t.combines);
       res.stats.depth = std::max(res.stats.depth, t.depth);
       reduce3(sm, eta_a, eta_b);
-      const unsigned long long key2 = fetch_error(ctx);
-      if (key2 != ~0ull)
-        throw ApiError(PODE_ERR_SINGULAR_FACTOR, "ieks iteration " + std::to_string(it) +
-                                                     ": smoother: triangular factor is singular",
-                       int64_t(key2 >> 8), 0.0, it);
+      check_linearization(ctx, s, it);
       const double v = 0.5 * ctx->h_scalars[0];
       const double dmax = ctx->h_scalars[1], emax = ctx->h_scalars[2];
       res.trace.push_back(v);
@@ -406,25 +493,7 @@ struct IeksEngine {
       }
     }
     res.iterations = it;
-    // calibration from the final pass' innovations
-    double* vals = ws.arr<double>("ieks_innov", N);
-    k_innovation<D><<<blocks_for<D>(N), kThreads, smem_bytes<D>(), st>>>(ch, fm, fc, vals, err);
-    note_launch(ctx, "innovation");
-    const int64_t np2 = grid1(N);
-    double* part2 = ws.arr<double>("ieks_part2", np2 * 3 + 3);
-    k_sum_blocks<<<np2, kRedThreads, 0, st>>>(vals, N, part2);
-    note_launch(ctx, "sum_blocks");
-    k_finish3<<<1, kRedThreads, 0, st>>>(part2, np2, part2 + np2 * 3);
-    note_launch(ctx, "finish3");
-    double sq = 0.0;
-    cuda_check(cudaMemcpyAsync(&sq, part2 + np2 * 3, sizeof(double), cudaMemcpyDeviceToHost, st), "innov");
-    cuda_check(cudaStreamSynchronize(st), "sync");
-    const int64_t count = N * dim;
-    const double sigma_rel = std::sqrt(sq / double(count));
-    res.sigma_hat = sigma_rel * prior.sigma;
-    k_outputs<<<grid1(n1), kRedThreads, 0, st>>>(eta_a, sc, scale, sigma_rel, n1, D, nu, dim, means, cov, sol_m,
-                                                 sol_c);
-    note_launch(ctx, "outputs");
+    finalize(ctx, s, eta_b, eta_a, cfg.linearization, it, prior.sigma, means, cov, sol_m, sol_c, res);
     return res;
   }
 };

@@ -1,6 +1,10 @@
 // Instantiates the engine for one state dimension; included by inst_dN.cu
 // with PODE_D defined, so the per-D kernels compile in parallel.
+#include <cstdlib>
+#include <string>
+
 #include "dispatch.hpp"
+#include "fast_driver.cuh"
 #include "ieks.cuh"
 
 #ifndef PODE_D
@@ -31,8 +35,40 @@ void ss(pode_context* c, int64_t n, const SEd& i, const SEd& o, bool rev, ScanTa
 void rt(pode_context* c, const DevChain& ch, double* fm, double* fc, double* sm, double* sc, ScanTally* t) {
   *t = E::rts(c, ch, fm, fc, sm, sc);
 }
+template <int DD, int d>
+constexpr bool kFastOk = (d <= 3) && (DD % d == 0) && (DD / d >= 2) && (DD / d <= 5);
+
+// The fused engine (fast.cuh) serves ODE information operators with d <= 3;
+// everything else (and PODE_IEKS_ENGINE=elements) runs the element/scan
+// engine with the reference's per-iteration structure.
 void ik(pode_context* c, const host::Problem& p, const pode_prior& pr, const double* g, int64_t n1,
         const pode_ieks_config& cfg, double* m, double* cv, double* sm, double* sc, IeksResult* out) {
+  const char* env = std::getenv("PODE_IEKS_ENGINE");
+  const bool elements = env != nullptr && std::string(env) == "elements";
+  if (!elements) {
+    switch (pr.dim) {
+      case 1:
+        if constexpr (kFastOk<kD, 1>) {
+          *out = FastEngine<kD, 1>::run(c, p, pr, g, n1, cfg, m, cv, sm, sc);
+          return;
+        }
+        break;
+      case 2:
+        if constexpr (kFastOk<kD, 2>) {
+          *out = FastEngine<kD, 2>::run(c, p, pr, g, n1, cfg, m, cv, sm, sc);
+          return;
+        }
+        break;
+      case 3:
+        if constexpr (kFastOk<kD, 3>) {
+          *out = FastEngine<kD, 3>::run(c, p, pr, g, n1, cfg, m, cv, sm, sc);
+          return;
+        }
+        break;
+      default:
+        break;
+    }
+  }
   *out = IeksEngine<kD>::run(c, p, pr, g, n1, cfg, m, cv, sm, sc);
 }
 const EngineOps kOps{kD, cf, cs, mf, ms, sf, ss, rt, ik};

@@ -230,7 +230,10 @@ __device__ __forceinline__ bool combine_filtering(const Grp<D>& g, const FEl<D>&
     bot[j] = rj.j[j];
     bot[D + j] = 0.0;
   }
-  lq<D, D, D, K>(g, top, bot);
+  // Only the first D pivots are needed: they give Xi11 and Xi21, and the
+  // remaining bottom block R satisfies R R^T = Xi22 Xi22^T (any factor of
+  // Xi22 serves, since it only enters J through another tria).
+  lq<D, D, 0, K>(g, top, bot);
   const bool sing = singular_diag(g, pick(top, g.r), D);
   Rw<D> xi11, xi21, xi22;
 #pragma unroll
@@ -250,15 +253,28 @@ __device__ __forceinline__ bool combine_filtering(const Grp<D>& g, const FEl<D>&
   const double t1 = matvec_t(g, li.c, rj.eta);
   const double t2 = matvec(g, li.c, t1);
   out.b = matvec(g, ag, li.b + t2) + rj.b;
-  // C = tria([A_j W, C_j])
-  out.c = sqrt_sum(g, mm(g, rj.a, w), rj.c);
   // eta = A_i^T G^T (eta_j - J_j (J_j^T b_i)) + eta_i = (G A_i)^T (...) + eta_i
   const double u1 = matvec_t(g, rj.j, li.b);
   const double u2 = matvec(g, rj.j, u1);
   const Rw<D> ga = mm(g, gm, li.a);
   out.eta = matvec_t(g, ga, rj.eta - u2) + li.eta;
-  // J = tria([A_i^T Xi22, J_i])
-  out.j = sqrt_sum(g, mm_tn(g, li.a, xi22), li.j);
+  // C = tria([A_j W, C_j]) and J = tria([A_i^T Xi22, J_i]) in one sweep.
+  const Rw<D> aw = mm(g, rj.a, w);
+  const Rw<D> ax = mm_tn(g, li.a, xi22);
+  Rw<2 * D> sc_c, sc_j;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    sc_c[j] = aw[j];
+    sc_c[D + j] = rj.c[j];
+    sc_j[j] = ax[j];
+    sc_j[D + j] = li.j[j];
+  }
+  lq_pair<D, 2 * D>(g, sc_c, sc_j);
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    out.c[j] = sc_c[j];
+    out.j[j] = sc_j[j];
+  }
   return !sing;
 }
 
