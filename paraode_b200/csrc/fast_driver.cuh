@@ -4,10 +4,13 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "fast.cuh"
 #include "ieks.cuh"
+#include "lane.cuh"
 
 namespace pode {
 
@@ -24,8 +27,18 @@ struct FastEngine {
     cudaFuncSetAttribute(k_fast_bwd_down<D, d, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   }
 
+  static bool lane_mode() {
+    const char* env = std::getenv("PODE_FAST_MODE");
+    return !(env != nullptr && std::string(env) == "group");
+  }
+
   // Chunk length: enough chunks to fill every SM with resident groups.
   static int chunk_len(pode_context* ctx, int64_t N) {
+    if (lane_mode()) {  // one chunk per thread, ~256 resident threads per SM
+      const int64_t target = int64_t(ctx->sm_count) * 256;
+      const int64_t L = (N + target - 1) / target;
+      return static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(L, 4096)));
+    }
     const int64_t target = int64_t(ctx->sm_count) * 16 * Grp<D>::kPerWarp;
     const int64_t L = (N + target - 1) / target;
     return static_cast<int>(std::max<int64_t>(4, std::min<int64_t>(L, 4096)));
@@ -63,21 +76,28 @@ struct FastEngine {
       double* base = ws.arr<double>("fast_bagg", size_t(nc) * (D * D + D));
       bagg = SEd{base, base + size_t(nc) * D * D, nullptr};
     }
-    double* part = ws.arr<double>("fast_part", nc * 3 + 3);
-    double* red = part + nc * 3;
+    const bool lanes = lane_mode();
+    const unsigned lblocks = static_cast<unsigned>((nc + lane::kLaneThreads - 1) / lane::kLaneThreads);
+    const int64_t nparts = lanes ? int64_t(lblocks) : nc;
+    double* part = ws.arr<double>("fast_part", nparts * 3 + 3);
+    double* red = part + nparts * 3;
     const unsigned blocks = blocks_for<D>(nc);
     const size_t sm = smem_bytes<D>();
 
     k_fill_rows<<<grid1(n1 * D), kRedThreads, 0, st>>>(s.mu0, n1, D, eta_a);
     note_launch(ctx, "fill");
     auto finish = [&]() {
-      k_finish3<<<1, kRedThreads, 0, st>>>(part, nc, red);
+      k_finish3<<<1, kRedThreads, 0, st>>>(part, nparts, red);
       note_launch(ctx, "finish3");
       cuda_check(cudaMemcpyAsync(ctx->h_scalars, red, sizeof(double) * 3, cudaMemcpyDeviceToHost, st), "red");
     };
     // objective of the constant start (ieks.cpp:147-148)
     a.eta = eta_a;
-    k_fast_bwd_down<D, d, true><<<blocks, kThreads, sm, st>>>(a, cst, elems, bagg, eta_a, eta_b, part);
+    if (lanes)
+      lane::k_lane_bwd_down<D, d, true><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, elems, bagg, eta_a, eta_b,
+                                                                               part);
+    else
+      k_fast_bwd_down<D, d, true><<<blocks, kThreads, sm, st>>>(a, cst, elems, bagg, eta_a, eta_b, part);
     note_launch(ctx, "fast_objective");
     finish();
     cuda_check(cudaStreamSynchronize(st), "sync");
@@ -89,13 +109,23 @@ struct FastEngine {
       ++it;
       reset_error(ctx);
       a.eta = eta_a;
-      k_fast_fwd_reduce<D, d><<<blocks, kThreads, sm, st>>>(a, cst, agg);
+      if (lanes)
+        lane::k_lane_fwd_reduce<D, d><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, agg);
+      else
+        k_fast_fwd_reduce<D, d><<<blocks, kThreads, sm, st>>>(a, cst, agg);
       note_launch(ctx, "fast_fwd_reduce");
       const ScanTally tf = Engine<D>::scan_filtering(ctx, nc, agg, agg, false);
-      k_fast_fwd_down<D, d><<<blocks, kThreads, sm, st>>>(a, cst, agg, elems, bagg);
+      if (lanes)
+        lane::k_lane_fwd_down<D, d><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, agg, elems, bagg);
+      else
+        k_fast_fwd_down<D, d><<<blocks, kThreads, sm, st>>>(a, cst, agg, elems, bagg);
       note_launch(ctx, "fast_fwd_down");
       const ScanTally tr = Engine<D>::scan_means_reverse(ctx, nc, bagg);
-      k_fast_bwd_down<D, d, false><<<blocks, kThreads, sm, st>>>(a, cst, elems, bagg, eta_a, eta_b, part);
+      if (lanes)
+        lane::k_lane_bwd_down<D, d, false><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, elems, bagg, eta_a,
+                                                                                  eta_b, part);
+      else
+        k_fast_bwd_down<D, d, false><<<blocks, kThreads, sm, st>>>(a, cst, elems, bagg, eta_a, eta_b, part);
       note_launch(ctx, "fast_bwd_down");
       finish();
       IE::check_linearization(ctx, s, it);  // syncs the stream

@@ -1,0 +1,728 @@
+// Lane-serial small-matrix fp64 kernels: one time-chunk (or one scan
+// element) per THREAD, every matrix in registers, no cross-lane traffic.
+//
+// Why: a square-root Kalman step at D <= 8 is ~10^3 FMAs of short, mostly
+// independent row updates.  Spreading one step over D lanes (group.cuh)
+// costs ~3x more shuffle / shared-memory / select instructions than FMAs and
+// leaves every lane waiting on the pivot chain; running 32 independent
+// chunks per warp instead keeps the FP64 pipe fed with pure DFMA streams and
+// needs no synchronisation at all.  Register pressure is the price; spills
+// (if any) stay in L1.
+//
+// Algebra restated (row form of Eigen's Householder QR of the transpose,
+// proj/src/linalg.cpp:9-27): kf_predict / kf_update (sequential.cpp:30-67),
+// make_filtering_element + ⊗_f (parallel.cpp:5-100), make_smoothing_element
+// (parallel.cpp:112-135), ⊗_s on (E, g) (parallel.cpp:146-156).
+#pragma once
+
+#include <cfloat>
+
+#include "engine.cuh"
+#include "field.cuh"
+#include "fast.cuh"
+
+namespace pode {
+namespace lane {
+
+constexpr int kLaneThreads = 128;
+
+// Householder LQ of an R x K row-major register matrix over the first P
+// pivots: row p is reflected against columns p..K-1 and every later row is
+// updated (Eigen convention: beta = -sign(c0) ||x||, tau = (beta - c0) / beta,
+// essential = tail / (c0 - beta); identity when ||tail||^2 <= DBL_MIN).
+template <int R, int K, int P>
+__device__ __forceinline__ void lq(double (&m)[R][K]) {
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+    for (int j = p + 1; j < K; ++j) {
+      if ((j - p) & 1)
+        t0 = fma(m[p][j], m[p][j], t0);
+      else
+        t1 = fma(m[p][j], m[p][j], t1);
+    }
+    const double tail = t0 + t1;
+    const double c0 = m[p][p];
+    if (tail > DBL_MIN) {
+      double beta = sqrt(fma(c0, c0, tail));
+      beta = (c0 >= 0.0) ? -beta : beta;
+      const double inv = __drcp_rn(c0 - beta);
+      const double tau = (beta - c0) * __drcp_rn(beta);
+      double ess[K];
+#pragma unroll
+      for (int j = p + 1; j < K; ++j) ess[j] = m[p][j] * inv;
+#pragma unroll
+      for (int r = p + 1; r < R; ++r) {
+        double w0 = m[r][p], w1 = 0.0;
+#pragma unroll
+        for (int j = p + 1; j < K; ++j) {
+          if ((j - p) & 1)
+            w1 = fma(m[r][j], ess[j], w1);
+          else
+            w0 = fma(m[r][j], ess[j], w0);
+        }
+        const double tw = tau * (w0 + w1);
+        m[r][p] -= tw;
+#pragma unroll
+        for (int j = p + 1; j < K; ++j) m[r][j] = fma(-tw, ess[j], m[r][j]);
+      }
+      m[p][p] = beta;
+#pragma unroll
+      for (int j = p + 1; j < K; ++j) m[p][j] = 0.0;
+    }
+  }
+}
+
+template <int D>
+__device__ __forceinline__ bool singular_diag(const double (&l)[D][D], int n) {
+  double mx = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+    if (i < n) mx = fmax(mx, fabs(l[i][i]));
+  bool s = false;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+    if (i < n) s |= fabs(l[i][i]) <= 1e-13 * mx;
+  return s;
+}
+
+// The transition's block structure: phi_n = phi_bar diag(ratio), phi_bar
+// block-diagonal binomial (prior.cpp:99-107; ieks.cpp:37-45).
+template <int D, int d>
+struct Model {
+  static constexpr int B = D / d;
+  static constexpr int q = B - 1;
+
+  __device__ static double binom(int n, int k) {
+    double num = 1.0, den = 1.0;
+    for (int t = 0; t < k; ++t) {
+      num *= double(n - t);
+      den *= double(t + 1);
+    }
+    return num / den;
+  }
+
+  // phi entry (a -> i within a block) = phi_bar[a][i] * ratio[i]
+  __device__ static void phi_coefs(const double (&ratio)[B], double (&pc)[B][B]) {
+#pragma unroll
+    for (int a = 0; a < B; ++a)
+#pragma unroll
+      for (int i = 0; i < B; ++i) pc[a][i] = (i >= a) ? binom(q - a, i - a) * ratio[i] : 0.0;
+  }
+
+  // y = phi x (in place safe: row a of a block reads rows >= a).
+  template <int K>
+  __device__ static void phi_rows(const double (&pc)[B][B], double (&x)[D][K]) {
+#pragma unroll
+    for (int blk = 0; blk < d; ++blk)
+#pragma unroll
+      for (int a = 0; a < B; ++a) {
+        double o[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) o[j] = pc[a][a] * x[blk * B + a][j];
+#pragma unroll
+        for (int i = a + 1; i < B; ++i)
+#pragma unroll
+          for (int j = 0; j < K; ++j) o[j] = fma(pc[a][i], x[blk * B + i][j], o[j]);
+#pragma unroll
+        for (int j = 0; j < K; ++j) x[blk * B + a][j] = o[j];
+      }
+  }
+
+  __device__ static void phi_vec(const double (&pc)[B][B], double (&x)[D]) {
+#pragma unroll
+    for (int blk = 0; blk < d; ++blk)
+#pragma unroll
+      for (int a = 0; a < B; ++a) {
+        double o = pc[a][a] * x[blk * B + a];
+#pragma unroll
+        for (int i = a + 1; i < B; ++i) o = fma(pc[a][i], x[blk * B + i], o);
+        x[blk * B + a] = o;
+      }
+  }
+
+  // Linearisation (statespace.cpp:65-103) at the full state eta (original
+  // coordinates); H_bar row i = (E_1 - F_y E_0)[i] diag(T_{n}).
+  struct Lin {
+    double jac[d][d];
+    double off[d];
+    bool finite;
+  };
+  __device__ static Lin linearize(const DevProblem& prob, const double* eta, int ek0) {
+    Lin l;
+    double y[d], f[d], jac[d * d];
+#pragma unroll
+    for (int j = 0; j < d; ++j) y[j] = eta[j * B];
+    eval_field<d>(prob, y, f, jac);
+    bool fin = true;
+#pragma unroll
+    for (int j = 0; j < d; ++j) fin &= isfinite(f[j]);
+#pragma unroll
+    for (int i = 0; i < d; ++i)
+#pragma unroll
+      for (int j = 0; j < d; ++j) {
+        if (!ek0) fin &= isfinite(jac[i * d + j]);
+        l.jac[i][j] = ek0 ? 0.0 : jac[i * d + j];
+      }
+    l.finite = fin;
+#pragma unroll
+    for (int i = 0; i < d; ++i) {
+      double jy = 0.0;
+#pragma unroll
+      for (int j = 0; j < d; ++j) jy += l.jac[i][j] * y[j];
+      l.off[i] = ek0 ? f[i] : f[i] - jy;
+    }
+    return l;
+  }
+
+  // rows of H_bar X (d x K)
+  template <int K>
+  __device__ static void h_rows(const Lin& l, const double (&t)[B], const double (&x)[D][K], double (&o)[d][K]) {
+#pragma unroll
+    for (int i = 0; i < d; ++i) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) o[i][j] = (1.0 * t[1]) * x[i * B + 1][j];
+#pragma unroll
+      for (int c = 0; c < d; ++c) {
+        const double coef = (-l.jac[i][c]) * t[0];
+#pragma unroll
+        for (int j = 0; j < K; ++j) o[i][j] = fma(coef, x[c * B][j], o[i][j]);
+      }
+    }
+  }
+  __device__ static void h_vec(const Lin& l, const double (&t)[B], const double (&x)[D], double (&o)[d]) {
+#pragma unroll
+    for (int i = 0; i < d; ++i) {
+      double v = (1.0 * t[1]) * x[i * B + 1];
+#pragma unroll
+      for (int c = 0; c < d; ++c) v = fma((-l.jac[i][c]) * t[0], x[c * B], v);
+      o[i] = v;
+    }
+  }
+
+  // Square-root update against the noiseless d-row observation
+  // (sequential.cpp:41-67, R = 0): Psi = tria([[H C-], [C-]]) over D
+  // columns.  Produces S (d x d), the gain K (D x d) and C+ (in cm).
+  struct Upd {
+    double s[d][d];
+    double sinv[d];
+    double k[D][d];
+    bool singular;
+  };
+  __device__ static Upd update(const Lin& l, const double (&t)[B], double (&cm)[D][D]) {
+    Upd u;
+    double psi[d + D][D];
+    double hc[d][D];
+    h_rows<D>(l, t, cm, hc);
+#pragma unroll
+    for (int i = 0; i < d; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) psi[i][j] = hc[i][j];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int j = 0; j < D; ++j) psi[d + r][j] = cm[r][j];
+    lq<d + D, D, D>(psi);
+    double mx = 0.0;
+#pragma unroll
+    for (int i = 0; i < d; ++i) mx = fmax(mx, fabs(psi[i][i]));
+    bool sg = false;
+#pragma unroll
+    for (int i = 0; i < d; ++i) {
+      sg |= fabs(psi[i][i]) <= 1e-13 * mx;
+#pragma unroll
+      for (int j = 0; j < d; ++j) u.s[i][j] = (j <= i) ? psi[i][j] : 0.0;
+      u.sinv[i] = __drcp_rn(psi[i][i]);
+    }
+    u.singular = sg;
+    // K = Psi21 S^-1 (x S = Psi21[r]) ; C+ = Psi22 (shifted by d columns)
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+#pragma unroll
+      for (int i = d - 1; i >= 0; --i) {
+        double acc = psi[d + r][i];
+#pragma unroll
+        for (int k = i + 1; k < d; ++k) acc = fma(-u.k[r][k], u.s[k][i], acc);
+        u.k[r][i] = acc * u.sinv[i];
+      }
+#pragma unroll
+      for (int j = 0; j < D; ++j) cm[r][j] = (j < D - d) ? psi[d + r][d + j] : 0.0;
+    }
+    return u;
+  }
+
+  __device__ static void s_solve(const Upd& u, const double (&v)[d], double (&w)[d]) {
+#pragma unroll
+    for (int i = 0; i < d; ++i) {
+      double acc = v[i];
+#pragma unroll
+      for (int k = 0; k < i; ++k) acc = fma(-u.s[i][k], w[k], acc);
+      w[i] = acc * u.sinv[i];
+    }
+  }
+
+  // C- = tria([phi C, Q]) (kf_predict, sequential.cpp:30-39); on return
+  // pm holds phi C (before the sweep, for callers that need it).
+  __device__ static void predict_cov(const double (&pc)[B][B], const double (&c)[D][D], const double* qrow,
+                                     double (&cm)[D][D]) {
+    double m[D][2 * D];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        m[r][j] = c[r][j];
+        m[r][D + j] = qrow[r * D + j];
+      }
+    // phi acts on the left half
+    double left[D][D];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int j = 0; j < D; ++j) left[r][j] = m[r][j];
+    phi_rows<D>(pc, left);
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int j = 0; j < D; ++j) m[r][j] = left[r][j];
+    lq<D, 2 * D, D>(m);
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int j = 0; j < D; ++j) cm[r][j] = (j <= r) ? m[r][j] : 0.0;
+  }
+
+  __device__ static void taus(const double* grid, int64_t n, double (&t)[B], double (&ti)[B]) {
+    const double h = (n == 0) ? grid[1] - grid[0] : grid[n] - grid[n - 1];
+    const double rh = sqrt(h);
+    double fact = 1.0;
+#pragma unroll
+    for (int i = q; i >= 0; --i) {
+      const int k = q - i;
+      if (k > 0) fact *= k;
+      t[i] = rh * ipow(h, k) / fact;
+      ti[i] = 1.0 / t[i];
+    }
+  }
+};
+
+template <int D>
+__device__ __forceinline__ void ld_mat(const double* p, double (&m)[D][D]) {
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int j = 0; j < D; ++j) m[r][j] = p[r * D + j];
+}
+template <int D>
+__device__ __forceinline__ void st_mat(double* p, const double (&m)[D][D]) {
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int j = 0; j < D; ++j) p[r * D + j] = m[r][j];
+}
+
+// ------------------------------------------------------------- pass A ---
+// One thread per chunk: fold the chunk's filtering elements into the
+// aggregate (A, b, C, eta, J) (see fast.cuh for the algebra).
+template <int D, int d>
+__global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(FastArgs a, FastConst<D> cst, FEd agg) {
+  using M = Model<D, d>;
+  constexpr int B = M::B;
+  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (c >= a.nchunks) return;
+  const int64_t s = c * a.L;
+  const int64_t e = min(a.N, s + a.L);
+  double A[D][D], C[D][D], J[D][D], b[D], eta[D];
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      A[r][j] = (c != 0 && r == j) ? 1.0 : 0.0;
+      C[r][j] = 0.0;
+      J[r][j] = 0.0;
+    }
+    b[r] = (c == 0) ? cst.m0[r] : 0.0;
+    eta[r] = 0.0;
+  }
+  double tk[B], tki[B];
+  M::taus(a.grid, s, tk, tki);
+  bool bad_sing = false;
+  int64_t bad_lin = -1;
+  for (int64_t k = s; k < e; ++k) {
+    double tn[B], tni[B], ratio[B], pc[B][B];
+    M::taus(a.grid, k + 1, tn, tni);
+#pragma unroll
+    for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
+    M::phi_coefs(ratio, pc);
+    // predict
+    M::template phi_rows<D>(pc, A);
+    M::phi_vec(pc, b);
+    double cm[D][D];
+    M::predict_cov(pc, C, cst.q, cm);
+    // update at node k+1
+    const typename M::Lin lin = M::linearize(a.prob, a.eta + (k + 1) * D, a.ek0);
+    if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
+    const typename M::Upd u = M::update(lin, tn, cm);
+    bad_sing |= u.singular;
+    double U[d][D], uu[d];
+    M::template h_rows<D>(lin, tn, A, U);
+    M::h_vec(lin, tn, b, uu);
+#pragma unroll
+    for (int i = 0; i < d; ++i) uu[i] -= lin.off[i];
+    // A+ = A- - K U, b+ = b- - K u
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+#pragma unroll
+      for (int i = 0; i < d; ++i) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) A[r][j] = fma(-u.k[r][i], U[i][j], A[r][j]);
+        b[r] = fma(-u.k[r][i], uu[i], b[r]);
+      }
+    }
+    // Ubar = S^-1 U, ubar = S^-1 u; eta -= Ubar^T ubar; J = tria([J, Ubar^T])
+    double ub[d], X[D][d];
+    M::s_solve(u, uu, ub);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double col[d], w[d];
+#pragma unroll
+      for (int i = 0; i < d; ++i) col[i] = U[i][j];
+      M::s_solve(u, col, w);
+      double de = 0.0;
+#pragma unroll
+      for (int i = 0; i < d; ++i) {
+        X[j][i] = w[i];
+        de = fma(w[i], ub[i], de);
+      }
+      eta[j] -= de;
+    }
+    // structured Householder sweep: row p of [J | X] is nonzero only in
+    // columns <= p and the d extra columns.
+#pragma unroll
+    for (int p = 0; p < D; ++p) {
+      double tail = 0.0;
+#pragma unroll
+      for (int i = 0; i < d; ++i) tail = fma(X[p][i], X[p][i], tail);
+      const double c0 = J[p][p];
+      if (tail > DBL_MIN) {
+        double beta = sqrt(fma(c0, c0, tail));
+        beta = (c0 >= 0.0) ? -beta : beta;
+        const double inv = __drcp_rn(c0 - beta);
+        const double tau = (beta - c0) * __drcp_rn(beta);
+        double ess[d];
+#pragma unroll
+        for (int i = 0; i < d; ++i) ess[i] = X[p][i] * inv;
+#pragma unroll
+        for (int r = p + 1; r < D; ++r) {
+          double w = J[r][p];
+#pragma unroll
+          for (int i = 0; i < d; ++i) w = fma(X[r][i], ess[i], w);
+          const double tw = tau * w;
+          J[r][p] -= tw;
+#pragma unroll
+          for (int i = 0; i < d; ++i) X[r][i] = fma(-tw, ess[i], X[r][i]);
+        }
+        J[p][p] = beta;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int j = 0; j < D; ++j) C[r][j] = cm[r][j];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      tk[i] = tn[i];
+      tki[i] = tni[i];
+    }
+  }
+  if (bad_lin >= 0) raise_error(a.err, bad_lin, kErrLinearization);
+  if (bad_sing) raise_error(a.err, s, kErrSingular);
+  st_mat<D>(agg.a + c * D * D, A);
+  st_mat<D>(agg.c + c * D * D, C);
+  st_mat<D>(agg.j + c * D * D, J);
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    agg.b[c * D + r] = b[r];
+    agg.eta[c * D + r] = eta[r];
+  }
+}
+
+// ------------------------------------------------------------- pass C ---
+// One thread per chunk: square-root Kalman filter from the chunk's incoming
+// filtered marginal; smoothing elements E_n, g_n (parallel.cpp:112-135) of
+// every node, and the chunk's backward aggregate (E, g).
+template <int D, int d>
+__global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, FastConst<D> cst, FEd prefix,
+                                                                SEd elems, SEd bagg) {
+  using M = Model<D, d>;
+  constexpr int B = M::B;
+  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (c >= a.nchunks) return;
+  const int64_t s = c * a.L;
+  const int64_t e = min(a.N, s + a.L);
+  double m[D], C[D][D], Eg[D][D], gg[D];
+  if (c == 0) {
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      m[r] = cst.m0[r];
+#pragma unroll
+      for (int j = 0; j < D; ++j) C[r][j] = 0.0;
+    }
+  } else {
+    ld_mat<D>(prefix.c + (c - 1) * D * D, C);
+#pragma unroll
+    for (int r = 0; r < D; ++r) m[r] = prefix.b[(c - 1) * D + r];
+  }
+  double tk[B], tki[B];
+  M::taus(a.grid, s, tk, tki);
+  bool bad_sing = false;
+  int64_t bad_lin = -1;
+  for (int64_t k = s; k < e; ++k) {
+    double tn[B], tni[B], ratio[B], pc[B][B];
+    M::taus(a.grid, k + 1, tn, tni);
+#pragma unroll
+    for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
+    M::phi_coefs(ratio, pc);
+    // Y = C (phi C)^T = C C^T phi^T; C- = tria([phi C, Q]); E = Y C-^-T C-^-1
+    double pcC[D][D];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int j = 0; j < D; ++j) pcC[r][j] = C[r][j];
+    M::template phi_rows<D>(pc, pcC);
+    double Y[D][D];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int x = 0; x <= r; ++x) acc = fma(C[r][x], pcC[j][x], acc);
+        Y[r][j] = acc;
+      }
+    double cm[D][D];
+    M::predict_cov(pc, C, cst.q, cm);
+    bad_sing |= singular_diag<D>(cm, D);
+    double rd[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) rd[i] = __drcp_rn(cm[i][i]);
+    double E[D][D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      double z[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {  // z C-^T = Y[r]  (forward)
+        double acc = Y[r][i];
+#pragma unroll
+        for (int k2 = 0; k2 < i; ++k2) acc = fma(-cm[i][k2], z[k2], acc);
+        z[i] = acc * rd[i];
+      }
+#pragma unroll
+      for (int i = D - 1; i >= 0; --i) {  // E[r] C- = z  (backward)
+        double acc = z[i];
+#pragma unroll
+        for (int k2 = i + 1; k2 < D; ++k2) acc = fma(-E[r][k2], cm[k2][i], acc);
+        E[r][i] = acc * rd[i];
+      }
+    }
+    double mm[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) mm[r] = m[r];
+    M::phi_vec(pc, mm);
+    double gk[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc = fma(E[r][j], mm[j], acc);
+      gk[r] = m[r] - acc;
+    }
+    st_mat<D>(elems.e + k * D * D, E);
+#pragma unroll
+    for (int r = 0; r < D; ++r) elems.g[k * D + r] = gk[r];
+    // backward aggregate in time order: (Eg, gg) <- (Eg E, Eg g_k + gg)
+    if (k == s) {
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        gg[r] = gk[r];
+#pragma unroll
+        for (int j = 0; j < D; ++j) Eg[r][j] = E[r][j];
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        double o[D], og = gg[r];
+#pragma unroll
+        for (int j = 0; j < D; ++j) o[j] = 0.0;
+#pragma unroll
+        for (int x = 0; x < D; ++x) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) o[j] = fma(Eg[r][x], E[x][j], o[j]);
+          og = fma(Eg[r][x], gk[x], og);
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j) Eg[r][j] = o[j];
+        gg[r] = og;
+      }
+    }
+    // measurement update at node k+1
+    const typename M::Lin lin = M::linearize(a.prob, a.eta + (k + 1) * D, a.ek0);
+    if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
+    const typename M::Upd u = M::update(lin, tn, cm);
+    bad_sing |= u.singular;
+    double z[d];
+    M::h_vec(lin, tn, mm, z);
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      double v = mm[r];
+#pragma unroll
+      for (int i = 0; i < d; ++i) v = fma(-u.k[r][i], z[i] - lin.off[i], v);
+      m[r] = v;
+#pragma unroll
+      for (int j = 0; j < D; ++j) C[r][j] = cm[r][j];
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      tk[i] = tn[i];
+      tki[i] = tni[i];
+    }
+  }
+  if (e == a.N) {  // terminal node N: E = 0, g = m_f(N) (parallel.cpp:137-144)
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      double acc = gg[r];
+#pragma unroll
+      for (int x = 0; x < D; ++x) {
+        acc = fma(Eg[r][x], m[x], acc);
+        elems.e[(a.N * D + r) * D + x] = 0.0;
+      }
+      elems.g[a.N * D + r] = m[r];
+      gg[r] = acc;
+#pragma unroll
+      for (int j = 0; j < D; ++j) Eg[r][j] = 0.0;
+    }
+  }
+  if (bad_lin >= 0) raise_error(a.err, bad_lin, kErrLinearization);
+  if (bad_sing) raise_error(a.err, s, kErrSingular);
+  st_mat<D>(bagg.e + c * D * D, Eg);
+#pragma unroll
+  for (int r = 0; r < D; ++r) bagg.g[c * D + r] = gg[r];
+}
+
+// ------------------------------------------------------------- pass E ---
+// One thread per chunk: backward mean recursion m_n = g_n + E_n m_{n+1}
+// from the chunk's incoming smoothed mean; new trajectory (original
+// coordinates) and per-chunk objective / stopping partials.
+template <int D, int d, bool kInitial>
+__global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, FastConst<D> cst, SEd elems,
+                                                                SEd suffix, const double* eta_old,
+                                                                double* eta_new, double* part) {
+  using M = Model<D, d>;
+  constexpr int B = M::B;
+  __shared__ double red[3][kLaneThreads];
+  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const bool okc = c < a.nchunks;
+  double obj = 0.0, dmax = 0.0, emax = 0.0;
+  if (okc) {
+    const int64_t s = c * a.L;
+    const int64_t e = min(a.N, s + a.L);
+    const bool last = c == a.nchunks - 1;
+    double mu[D], te[B], tei[B];
+    M::taus(a.grid, e, te, tei);
+    double bar_next[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      double eta_e;
+      if (kInitial) {
+        eta_e = eta_old[e * D + r];
+        mu[r] = 0.0;
+      } else {
+        mu[r] = last ? elems.g[a.N * D + r] : suffix.g[(c + 1) * D + r];
+        eta_e = te[r % B] * mu[r];
+      }
+      if (last) {
+        if (!kInitial) eta_new[a.N * D + r] = eta_e;
+        dmax = fmax(dmax, fabs(eta_e - eta_old[a.N * D + r]));
+        emax = fmax(emax, fabs(eta_e));
+      }
+      bar_next[r] = tei[r % B] * eta_e;
+    }
+    double tn[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) tn[i] = tei[i];  // T_{k+1}^-1
+    for (int64_t k = e - 1; k >= s; --k) {
+      double tk[B], tki[B];
+      M::taus(a.grid, k, tk, tki);
+      double etak[D];
+      if (kInitial) {
+#pragma unroll
+        for (int r = 0; r < D; ++r) etak[r] = eta_old[k * D + r];
+      } else {
+        double E[D][D], nm[D];
+        ld_mat<D>(elems.e + k * D * D, E);
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          double acc = elems.g[k * D + r];
+#pragma unroll
+          for (int j = 0; j < D; ++j) acc = fma(E[r][j], mu[j], acc);
+          nm[r] = acc;
+        }
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          mu[r] = nm[r];
+          etak[r] = tk[r % B] * nm[r];
+          eta_new[k * D + r] = etak[r];
+        }
+      }
+      double bar[D];
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        dmax = fmax(dmax, fabs(etak[r] - eta_old[k * D + r]));
+        emax = fmax(emax, fabs(etak[r]));
+        bar[r] = tki[r % B] * etak[r];
+      }
+      // objective term: || Qunit^-1/2 (bar_{k+1} - phi_k bar_k) ||^2
+      double ratio[B], pc[B][B], pb[D];
+#pragma unroll
+      for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tn[i];
+      M::phi_coefs(ratio, pc);
+#pragma unroll
+      for (int r = 0; r < D; ++r) pb[r] = bar[r];
+      M::phi_vec(pc, pb);
+      double w[D], acc2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double acc = bar_next[i] - pb[i];
+#pragma unroll
+        for (int k2 = 0; k2 < i; ++k2) acc = fma(-cst.qunit[i * D + k2], w[k2], acc);
+        w[i] = acc * cst.qunit_rdiag[i];
+        acc2 = fma(w[i], w[i], acc2);
+      }
+      obj += acc2;
+#pragma unroll
+      for (int r = 0; r < D; ++r) bar_next[r] = bar[r];
+#pragma unroll
+      for (int i = 0; i < B; ++i) tn[i] = tki[i];
+    }
+  }
+  red[0][threadIdx.x] = obj;
+  red[1][threadIdx.x] = dmax;
+  red[2][threadIdx.x] = emax;
+  __syncthreads();
+  for (int st = kLaneThreads / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + st];
+      red[1][threadIdx.x] = fmax(red[1][threadIdx.x], red[1][threadIdx.x + st]);
+      red[2][threadIdx.x] = fmax(red[2][threadIdx.x], red[2][threadIdx.x + st]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[blockIdx.x * 3 + 0] = red[0][0];
+    part[blockIdx.x * 3 + 1] = red[1][0];
+    part[blockIdx.x * 3 + 2] = red[2][0];
+  }
+}
+
+}  // namespace lane
+}  // namespace pode
