@@ -11,6 +11,7 @@
 #include "fast.cuh"
 #include "ieks.cuh"
 #include "lane.cuh"
+#include "lane_scan.cuh"
 
 namespace pode {
 
@@ -30,6 +31,15 @@ struct FastEngine {
   static bool lane_mode() {
     const char* env = std::getenv("PODE_FAST_MODE");
     return !(env != nullptr && std::string(env) == "group");
+  }
+  static bool lane_scans() {
+    const char* env = std::getenv("PODE_SCAN_MODE");
+    return !(env != nullptr && std::string(env) == "group");
+  }
+  static int scan_fanin() {
+    const char* env = std::getenv("PODE_SCAN_FANIN");
+    const int v = env ? std::atoi(env) : 4;
+    return v >= 2 ? v : 4;
   }
 
   // Chunk length: enough chunks to fill every SM with resident groups.
@@ -114,13 +124,22 @@ struct FastEngine {
       else
         k_fast_fwd_reduce<D, d><<<blocks, kThreads, sm, st>>>(a, cst, agg);
       note_launch(ctx, "fast_fwd_reduce");
-      const ScanTally tf = Engine<D>::scan_filtering(ctx, nc, agg, agg, false);
-      if (lanes)
-        lane::k_lane_fwd_down<D, d><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, agg, elems, bagg);
+      ScanTally tf, tr;
+      if (lane_scans())
+        lane::LaneScan<D, lane::LFOps<D>, false>::run(ctx, agg, agg, nc, 0, scan_fanin(), tf);
       else
+        tf = Engine<D>::scan_filtering(ctx, nc, agg, agg, false);
+      if (lanes) {
+        lane::k_lane_fwd_down<D, d><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, agg, elems, bagg);
+        note_launch(ctx, "lane_fwd_down");
+        lane::k_lane_bfold<D><<<lblocks, lane::kLaneThreads, 0, st>>>(elems, N, L, nc, bagg);
+      } else
         k_fast_fwd_down<D, d><<<blocks, kThreads, sm, st>>>(a, cst, agg, elems, bagg);
       note_launch(ctx, "fast_fwd_down");
-      const ScanTally tr = Engine<D>::scan_means_reverse(ctx, nc, bagg);
+      if (lane_scans())
+        lane::LaneScan<D, lane::LMOps<D>, true>::run(ctx, bagg, bagg, nc, 0, scan_fanin(), tr);
+      else
+        tr = Engine<D>::scan_means_reverse(ctx, nc, bagg);
       if (lanes)
         lane::k_lane_bwd_down<D, d, false><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, elems, bagg, eta_a,
                                                                                   eta_b, part);

@@ -247,7 +247,7 @@ struct Model {
         u.k[r][i] = acc * u.sinv[i];
       }
 #pragma unroll
-      for (int j = 0; j < D; ++j) cm[r][j] = (j < D - d) ? psi[d + r][d + j] : 0.0;
+      for (int j = 0; j < D; ++j) cm[r][j] = (j <= r && j < D - d) ? psi[d + r][d + j] : 0.0;
     }
     return u;
   }
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(FastArgs a, Fa
 #pragma unroll
     for (int r = 0; r < D; ++r)
 #pragma unroll
-      for (int j = 0; j < D; ++j) C[r][j] = cm[r][j];
+      for (int j = 0; j < D; ++j) C[r][j] = (j <= r) ? cm[r][j] : 0.0;
 #pragma unroll
     for (int i = 0; i < B; ++i) {
       tk[i] = tn[i];
@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
   if (c >= a.nchunks) return;
   const int64_t s = c * a.L;
   const int64_t e = min(a.N, s + a.L);
-  double m[D], C[D][D], Eg[D][D], gg[D];
+  double m[D], C[D][D];
   if (c == 0) {
 #pragma unroll
     for (int r = 0; r < D; ++r) {
@@ -540,31 +540,6 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
     st_mat<D>(elems.e + k * D * D, E);
 #pragma unroll
     for (int r = 0; r < D; ++r) elems.g[k * D + r] = gk[r];
-    // backward aggregate in time order: (Eg, gg) <- (Eg E, Eg g_k + gg)
-    if (k == s) {
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        gg[r] = gk[r];
-#pragma unroll
-        for (int j = 0; j < D; ++j) Eg[r][j] = E[r][j];
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        double o[D], og = gg[r];
-#pragma unroll
-        for (int j = 0; j < D; ++j) o[j] = 0.0;
-#pragma unroll
-        for (int x = 0; x < D; ++x) {
-#pragma unroll
-          for (int j = 0; j < D; ++j) o[j] = fma(Eg[r][x], E[x][j], o[j]);
-          og = fma(Eg[r][x], gk[x], og);
-        }
-#pragma unroll
-        for (int j = 0; j < D; ++j) Eg[r][j] = o[j];
-        gg[r] = og;
-      }
-    }
     // measurement update at node k+1
     const typename M::Lin lin = M::linearize(a.prob, a.eta + (k + 1) * D, a.ek0);
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
@@ -579,7 +554,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
       for (int i = 0; i < d; ++i) v = fma(-u.k[r][i], z[i] - lin.off[i], v);
       m[r] = v;
 #pragma unroll
-      for (int j = 0; j < D; ++j) C[r][j] = cm[r][j];
+      for (int j = 0; j < D; ++j) C[r][j] = (j <= r) ? cm[r][j] : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < B; ++i) {
@@ -590,20 +565,52 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
   if (e == a.N) {  // terminal node N: E = 0, g = m_f(N) (parallel.cpp:137-144)
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-      double acc = gg[r];
 #pragma unroll
-      for (int x = 0; x < D; ++x) {
-        acc = fma(Eg[r][x], m[x], acc);
-        elems.e[(a.N * D + r) * D + x] = 0.0;
-      }
+      for (int x = 0; x < D; ++x) elems.e[(a.N * D + r) * D + x] = 0.0;
       elems.g[a.N * D + r] = m[r];
-      gg[r] = acc;
-#pragma unroll
-      for (int j = 0; j < D; ++j) Eg[r][j] = 0.0;
     }
   }
   if (bad_lin >= 0) raise_error(a.err, bad_lin, kErrLinearization);
   if (bad_sing) raise_error(a.err, s, kErrSingular);
+  (void)bagg;
+}
+
+// Pass C2: one thread per chunk folds the chunk's smoothing elements in time
+// order into its backward aggregate, (E, g) <- (E E_n, E g_n + g)
+// (⊗_s on means, parallel.cpp:146-156); the last chunk includes the
+// terminal node N, so its aggregate has E = 0.
+template <int D>
+__global__ void __launch_bounds__(kLaneThreads) k_lane_bfold(SEd elems, int64_t N, int L, int64_t nchunks,
+                                                             SEd bagg) {
+  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (c >= nchunks) return;
+  const int64_t s = c * L;
+  const int64_t e = (c == nchunks - 1) ? N + 1 : min(N, s + L);
+  double Eg[D][D], gg[D];
+  ld_mat<D>(elems.e + s * D * D, Eg);
+#pragma unroll
+  for (int r = 0; r < D; ++r) gg[r] = elems.g[s * D + r];
+  for (int64_t k = s + 1; k < e; ++k) {
+    double E[D][D], gk[D];
+    ld_mat<D>(elems.e + k * D * D, E);
+#pragma unroll
+    for (int r = 0; r < D; ++r) gk[r] = elems.g[k * D + r];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      double o[D], og = gg[r];
+#pragma unroll
+      for (int j = 0; j < D; ++j) o[j] = 0.0;
+#pragma unroll
+      for (int x = 0; x < D; ++x) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) o[j] = fma(Eg[r][x], E[x][j], o[j]);
+        og = fma(Eg[r][x], gk[x], og);
+      }
+#pragma unroll
+      for (int j = 0; j < D; ++j) Eg[r][j] = o[j];
+      gg[r] = og;
+    }
+  }
   st_mat<D>(bagg.e + c * D * D, Eg);
 #pragma unroll
   for (int r = 0; r < D; ++r) bagg.g[c * D + r] = gg[r];
