@@ -236,7 +236,7 @@ struct Fast {
         const double v = __shfl_sync(0xffffffffu, top[j], lane0 + i);
         u.s[i][j] = (j <= i) ? v : 0.0;
       }
-      u.sinv[i] = __drcp_rn(u.s[i][i]);
+      u.sinv[i] = rcp_nr(u.s[i][i]);
     }
     // K = Psi21 S^-1 (row r: x S = Psi21[r, :], back substitution)
 #pragma unroll

@@ -32,9 +32,11 @@ struct FastEngine {
     const char* env = std::getenv("PODE_FAST_MODE");
     return !(env != nullptr && std::string(env) == "group");
   }
+  // Chunk-aggregate scans: the group engine by default (its ⊗_f has the
+  // shorter critical path); PODE_SCAN_MODE=lane selects the lane-serial one.
   static bool lane_scans() {
     const char* env = std::getenv("PODE_SCAN_MODE");
-    return !(env != nullptr && std::string(env) == "group");
+    return env != nullptr && std::string(env) == "lane";
   }
   static int scan_fanin() {
     const char* env = std::getenv("PODE_SCAN_FANIN");

@@ -255,21 +255,54 @@ struct Reflector {
   Rw<K> ess;  // ess[j], j > p
 };
 
+// Branch-free fp64 reciprocal square root and reciprocal: the MUFU
+// approximation refined by Newton steps to full double precision (no
+// IEEE slow-path calls, so a whole Householder sweep stays one basic block).
+// Inputs are positive normal numbers here (guarded by the callers).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  return y;
+}
+
+// Householder coefficients of x = [c0, tail] (Eigen's makeHouseholder):
+// beta = -sign(c0) ||x||, tau = (beta - c0) / beta, inv = 1 / (c0 - beta);
+// (tau, beta, inv) = (0, c0, 0) when ||tail||^2 <= DBL_MIN.  Branch-free.
+__device__ __forceinline__ void householder_coefs(double c0, double tail, double& tau, double& beta, double& inv) {
+  const bool live = tail > DBL_MIN;
+  const double n2 = fma(c0, c0, tail);
+  const double r = rsqrt_nr(live ? n2 : 1.0);  // 1 / ||x||
+  const double sgn = (c0 >= 0.0) ? -1.0 : 1.0;
+  const double b = sgn * (n2 * r);              // -sign(c0) ||x||
+  const double rb = sgn * r;                    // 1 / beta
+  const double ic = rcp_nr(live ? (c0 - b) : 1.0);
+  tau = live ? (b - c0) * rb : 0.0;
+  beta = live ? b : c0;
+  inv = live ? ic : 0.0;
+}
+
 template <int K>
 __device__ __forceinline__ Reflector<K> make_reflector(const Rw<K>& x, int p) {
   Reflector<K> h;
   const double tail = sumsq_from(x, p + 1);
-  const double c0 = x[p];
-  h.tau = 0.0;
-  h.beta = c0;
-  double inv = 0.0;
-  if (tail > DBL_MIN) {
-    double beta = sqrt(fma(c0, c0, tail));
-    beta = (c0 >= 0.0) ? -beta : beta;
-    inv = __drcp_rn(c0 - beta);
-    h.tau = (beta - c0) * __drcp_rn(beta);
-    h.beta = beta;
-  }
+  double inv;
+  householder_coefs(x[p], tail, h.tau, h.beta, inv);
 #pragma unroll
   for (int j = p + 1; j < K; ++j) h.ess[j] = x[j] * inv;
   return h;

@@ -43,34 +43,31 @@ __device__ __forceinline__ void lq(double (&m)[R][K]) {
         t1 = fma(m[p][j], m[p][j], t1);
     }
     const double tail = t0 + t1;
-    const double c0 = m[p][p];
-    if (tail > DBL_MIN) {
-      double beta = sqrt(fma(c0, c0, tail));
-      beta = (c0 >= 0.0) ? -beta : beta;
-      const double inv = __drcp_rn(c0 - beta);
-      const double tau = (beta - c0) * __drcp_rn(beta);
-      double ess[K];
+    double tau, beta, inv;
+    householder_coefs(m[p][p], tail, tau, beta, inv);  // branch-free (group.cuh)
+    double ess[K];
 #pragma unroll
-      for (int j = p + 1; j < K; ++j) ess[j] = m[p][j] * inv;
+    for (int j = p + 1; j < K; ++j) ess[j] = m[p][j] * inv;
 #pragma unroll
-      for (int r = p + 1; r < R; ++r) {
-        double w0 = m[r][p], w1 = 0.0;
+    for (int r = p + 1; r < R; ++r) {
+      double w0 = m[r][p], w1 = 0.0;
 #pragma unroll
-        for (int j = p + 1; j < K; ++j) {
-          if ((j - p) & 1)
-            w1 = fma(m[r][j], ess[j], w1);
-          else
-            w0 = fma(m[r][j], ess[j], w0);
-        }
-        const double tw = tau * (w0 + w1);
-        m[r][p] -= tw;
-#pragma unroll
-        for (int j = p + 1; j < K; ++j) m[r][j] = fma(-tw, ess[j], m[r][j]);
+      for (int j = p + 1; j < K; ++j) {
+        if ((j - p) & 1)
+          w1 = fma(m[r][j], ess[j], w1);
+        else
+          w0 = fma(m[r][j], ess[j], w0);
       }
-      m[p][p] = beta;
+      const double tw = tau * (w0 + w1);
+      m[r][p] -= tw;
 #pragma unroll
-      for (int j = p + 1; j < K; ++j) m[p][j] = 0.0;
+      for (int j = p + 1; j < K; ++j) m[r][j] = fma(-tw, ess[j], m[r][j]);
     }
+    // when tau == 0 (tail below DBL_MIN) this is the identity with beta = c0;
+    // the tail is dropped, as Eigen's triangular view of R drops it
+    m[p][p] = beta;
+#pragma unroll
+    for (int j = p + 1; j < K; ++j) m[p][j] = 0.0;
   }
 }
 
@@ -233,7 +230,7 @@ struct Model {
       sg |= fabs(psi[i][i]) <= 1e-13 * mx;
 #pragma unroll
       for (int j = 0; j < d; ++j) u.s[i][j] = (j <= i) ? psi[i][j] : 0.0;
-      u.sinv[i] = __drcp_rn(psi[i][i]);
+      u.sinv[i] = rcp_nr(psi[i][i]);
     }
     u.singular = sg;
     // K = Psi21 S^-1 (x S = Psi21[r]) ; C+ = Psi22 (shifted by d columns)
@@ -403,27 +400,22 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(FastArgs a, Fa
       double tail = 0.0;
 #pragma unroll
       for (int i = 0; i < d; ++i) tail = fma(X[p][i], X[p][i], tail);
-      const double c0 = J[p][p];
-      if (tail > DBL_MIN) {
-        double beta = sqrt(fma(c0, c0, tail));
-        beta = (c0 >= 0.0) ? -beta : beta;
-        const double inv = __drcp_rn(c0 - beta);
-        const double tau = (beta - c0) * __drcp_rn(beta);
-        double ess[d];
+      double tau, beta, inv;
+      householder_coefs(J[p][p], tail, tau, beta, inv);
+      double ess[d];
 #pragma unroll
-        for (int i = 0; i < d; ++i) ess[i] = X[p][i] * inv;
+      for (int i = 0; i < d; ++i) ess[i] = X[p][i] * inv;
 #pragma unroll
-        for (int r = p + 1; r < D; ++r) {
-          double w = J[r][p];
+      for (int r = p + 1; r < D; ++r) {
+        double w = J[r][p];
 #pragma unroll
-          for (int i = 0; i < d; ++i) w = fma(X[r][i], ess[i], w);
-          const double tw = tau * w;
-          J[r][p] -= tw;
+        for (int i = 0; i < d; ++i) w = fma(X[r][i], ess[i], w);
+        const double tw = tau * w;
+        J[r][p] -= tw;
 #pragma unroll
-          for (int i = 0; i < d; ++i) X[r][i] = fma(-tw, ess[i], X[r][i]);
-        }
-        J[p][p] = beta;
+        for (int i = 0; i < d; ++i) X[r][i] = fma(-tw, ess[i], X[r][i]);
       }
+      J[p][p] = beta;
     }
 #pragma unroll
     for (int r = 0; r < D; ++r)
@@ -505,7 +497,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
     bad_sing |= singular_diag<D>(cm, D);
     double rd[D];
 #pragma unroll
-    for (int i = 0; i < D; ++i) rd[i] = __drcp_rn(cm[i][i]);
+    for (int i = 0; i < D; ++i) rd[i] = rcp_nr(cm[i][i]);
     double E[D][D];
 #pragma unroll
     for (int r = 0; r < D; ++r) {

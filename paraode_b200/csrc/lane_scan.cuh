@@ -74,7 +74,7 @@ __device__ __noinline__ bool combine_f(const LF<D>& li, const LF<D>& rj, LF<D>& 
   const bool sing = singular_diag<D>(xi11, D);
   double rd[D];
 #pragma unroll
-  for (int i = 0; i < D; ++i) rd[i] = __drcp_rn(xi11[i][i]);
+  for (int i = 0; i < D; ++i) rd[i] = rcp_nr(xi11[i][i]);
   // W = C_i Xi11^-T  (row r: w Xi11^T = C_i[r], forward substitution)
   double w[D][D];
 #pragma unroll
