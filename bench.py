@@ -1,16 +1,16 @@
-"""Benchmark of the ParaIEKS hot path on B200 (see DESIGN.md §Measurement).
+"""Benchmark of the ParaIEKS hot path on B200 (DESIGN.md §Measurement).
 
-One "step" = one converged IEKS solve (FitzHugh–Nagumo, d=2, IWP(q=2),
-D=6, N=2^20 uniform steps on [0, 20]) — BASELINE.json configs[1] at its
-largest N.  value = time-steps/s over all ranks with the solve's inputs and
-outputs resident in HBM; e2e = the same metric through the public API with
-host buffers (grid H2D and the full SolverReport D2H inside the timed
-region).  `--impl reference` times the reference algorithm on the host
-cores (the C++ restatement in oracle/, the reference itself needs Eigen
-which this image lacks).
+One "step" = one IEKS solve to the reference's stopping rule (FitzHugh–Nagumo,
+d=2, IWP(q=2), D=6, N=2^20 uniform steps on [0, 20]; BASELINE.json
+configs[1] at its largest N).  value = time-steps/s over all ranks with the
+solve's outputs written to HBM; e2e = the same metric through the public
+Python API (paraode_b200.para_ieks) with host numpy buffers, so the grid
+upload and the full SolverReport download are inside the timed region.
+`--impl reference` times the reference algorithm on the host cores (the C++
+restatement in oracle/ — the reference itself needs Eigen, absent here).
 
 Multi-GPU: one process per GPU (torchrun); each rank solves its own
-independent problem (replicas, weak scaling) — see DESIGN.md §Multi-GPU.
+independent problem (replicas, weak scaling) — DESIGN.md §Multi-GPU.
 """
 import argparse
 import json
@@ -27,7 +27,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "IEKS wall-time to converged posterior; time-steps/s at N=2^20, 1/2/4/8 GPU"
-CPU_SAMPLE_N = 2 ** 13  # bounded CPU sample (full converged solve)
+CPU_SAMPLE_N = 2 ** 13  # bounded CPU sample: a full solve at reduced N
+HBM_FALLBACK_GBS = 6650.0
+FP64_FALLBACK_TFS = 36.6
 
 
 def parse():
@@ -44,19 +46,55 @@ def parse():
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def peaks():
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written HBM copy)
+    and profiles/r01_fp64_peak.json (our DFMA measurement on this pool)."""
+    hbm, hbm_src = HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+    try:
+        hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        hbm_src = "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        pass
+    fp64, fp64_src = FP64_FALLBACK_TFS, "fallback (nominal)"
+    try:
+        fp64 = float(json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")))["fp64_fma_tflops"])
+        fp64_src = "measured DFMA (profiles/r01_fp64_peak.json)"
+    except Exception:
+        pass
+    return hbm, hbm_src, fp64, fp64_src
+
+
+def f_lq(R, K, P):
+    """FMAs of a Householder LQ sweep over P pivots of an R x K row block."""
+    return sum(2 * (K - p - 1) + (R - p - 1) * 2 * (K - p) for p in range(P))
+
+
+def kernel_model(D, d):
+    """Algorithmic (flops, HBM bytes) per time step of the fused-iteration
+    kernels.  8-byte fp64 words."""
+    B = D // d
+    phi = d * B * (B + 1) // 2  # nonzeros of the block-binomial transition
+    upd = d * D * (d + 1) + f_lq(d + D, D, D) + D * d * d // 2 + D * d + d * (d + 1)
+    fwd_reduce = (2 * phi * D + phi + f_lq(D, 2 * D, D) + upd + d * D * (d + 1) + D * d * D + D * d
+                  + D * d * d + D * d + d * D * D)
+    fwd_down = phi * D + D * D * (D + 1) // 2 + f_lq(D, 2 * D, D) + D * D * D + D * D + phi + upd
+    return {
+        "fast_fwd_reduce": (2 * fwd_reduce, 8 * D),
+        "fast_fwd_down": (2 * fwd_down, 8 * (D + D * D + D)),
+        "fast_bwd_fold": (2 * (D ** 3 + D * D), 8 * (D * D + D)),
+        "fast_bwd_down": (2 * (D * D + phi + D * D // 2 + 2 * D), 8 * (D * D + D + 2 * D)),
+    }
 
 
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
     def __init__(self, index):
-        self.index = index
-        self.rows = []
-        self.proc = None
+        self.index, self.rows, self.proc = index, [], None
 
     def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -66,8 +104,7 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except FileNotFoundError:
             self.proc = None
         return self
@@ -95,21 +132,16 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_reference(args, problem_name, nu, n, steps, warmup, threads):
-    """The reference algorithm on the host cores (oracle/, the C++ restatement)."""
+def cpu_solve(problem_name, nu, n, threads):
+    """One full solve of the reference algorithm on the host (oracle/, the C++
+    restatement; mode 0 = seq_ieks on one thread, k > 1 = para_ieks on a
+    WorkPool(k))."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import _oracle as O
     prob = O.problem(problem_name)
     grid = O.uniform_grid(prob.t_end, n)
-    for _ in range(warmup):
-        O.ieks(prob, nu, grid, mode=threads, want_cov=True)
-    times, iters = [], 0
-    for _ in range(steps):
-        r = O.ieks(prob, nu, grid, mode=threads, want_cov=True)
-        times.append(r["seconds"])
-        iters = r["iterations"]
-    t = statistics.median(times)
-    return n / t, t, iters
+    r = O.ieks(prob, nu, grid, mode=threads, want_cov=True)
+    return r["seconds"], r["iterations"]
 
 
 def run_reference(args):
@@ -118,17 +150,22 @@ def run_reference(args):
         return
     threads = os.cpu_count() or 1
     n = CPU_SAMPLE_N
-    w = max(1, min(args.warmup, 1))
-    v, t, iters = cpu_reference(args, args.problem, args.nu, n, max(1, args.steps), w, threads)
-    cfg = {"workload": f"{args.problem} d=2 IWP(q={args.nu}) converged IEKS", "N": n,
-           "sample": "full converged solve at reduced N (the N=2^20 solve takes many minutes on CPU)",
-           "iterations": iters}
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_solve(args.problem, args.nu, n, threads)
+    times, iters = [], 0
+    for _ in range(max(1, args.steps)):
+        t, iters = cpu_solve(args.problem, args.nu, n, threads)
+        times.append(t)
+    t = statistics.median(times)
+    v = n / t
+    sample = f"para_ieks on WorkPool({threads}), full solve at N={n} ({iters} iterations)"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "time-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": cfg,
-            "cpu_baseline": {"value": v, "unit": "time-steps/s", "cores": threads, "kind": "port",
-                             "sample": f"para_ieks (WorkPool({threads})) on N={n}, {iters} iterations"},
+            "config": {"workload": f"{args.problem} d=2 IWP(q={args.nu}) D=6 IEKS to the reference stopping rule",
+                       "N": n, "iterations": iters,
+                       "note": "bounded sample at reduced N; the N=2^20 solve takes tens of minutes on CPU"},
+            "cpu_baseline": {"value": v, "unit": "time-steps/s", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "time-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -140,7 +177,10 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
+    import ctypes as C
+
     import paraode_b200 as P
+    from paraode_b200 import _abi as A
     ctx = P.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream)
     prob = P.problem_by_name(args.problem)
@@ -150,52 +190,56 @@ def run_ours(args):
     grid = P.uniform_grid(prob.t_end, n)
     n1 = n + 1
     dev = torch.device("cuda", local)
-    # device-resident outputs (value) and pinned host outputs (e2e)
     out_dev = [torch.empty((n1, D), dtype=torch.float64, device=dev),
                torch.empty((n1, D, D), dtype=torch.float64, device=dev),
                torch.empty((n1, d), dtype=torch.float64, device=dev),
                torch.empty((n1, d, d), dtype=torch.float64, device=dev)]
-    out_host = [torch.empty(t.shape, dtype=torch.float64, pin_memory=True) for t in out_dev]
     grid_pinned = torch.from_numpy(grid).pin_memory()
-    from paraode_b200 import _abi as A
-    import ctypes as C
+    cfg = P.IeksConfig()
 
-    def solve(location):
-        outs = out_dev if location == A.PODE_DEVICE else out_host
-        ptr = [C.cast(C.c_void_p(t.data_ptr()), A.dptr) for t in outs]
-        trace = np.zeros(256)
-        rep = A.IeksReport(ptr[0], ptr[1], ptr[2], ptr[3], trace.ctypes.data_as(A.dptr), 256, location,
-                           0, 0, 0.0, A.ScanStats())
+    def solve_device():
+        ptr = [C.cast(C.c_void_p(t.data_ptr()), A.dptr) for t in out_dev]
+        trace = np.zeros(cfg.max_iterations)
+        rep = A.IeksReport(ptr[0], ptr[1], ptr[2], ptr[3], trace.ctypes.data_as(A.dptr), cfg.max_iterations,
+                           A.PODE_DEVICE, 0, 0, 0.0, A.ScanStats())
         pr = prob._c()
         prior = A.Prior(nu, d, 1.0)
-        cfg = A.IeksConfig(100, 1e-13, 1e-9, 1e-6, 0)
+        c = A.IeksConfig(cfg.max_iterations, cfg.traj_rtol, cfg.obj_atol, cfg.obj_rtol, 0)
         st = A.Status()
         rc = ctx._lib.pode_ieks(ctx.handle, C.byref(pr), C.byref(prior),
-                                C.cast(C.c_void_p(grid_pinned.data_ptr()), A.dptr), n1, C.byref(cfg),
+                                C.cast(C.c_void_p(grid_pinned.data_ptr()), A.dptr), n1, C.byref(c),
                                 C.byref(rep), C.byref(st))
         P.api._raise(rc, st)
         return rep
 
+    def solve_public():
+        return P.para_ieks(prob, P.IwpPrior(nu, d, 1.0), grid, cfg, want_cov=True, ctx=ctx)
+
     for _ in range(args.warmup):
-        rep = solve(A.PODE_DEVICE)
-    iters = rep.iterations
+        rep = solve_device()
+    iters, converged = rep.iterations, bool(rep.converged)
+    solve_public()  # warm the host-buffer path too
 
     def barrier():
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
 
-    def timed(location):
+    def timed(fn, profile=False):
         barrier()
         torch.cuda.synchronize()
         l0 = ctx.kernel_launches
+        if profile:
+            ctx.profile(True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for _ in range(args.steps):
-                solve(location)
-            e1.record(stream)
+        e0.record(stream)
+        for _ in range(args.steps):
+            fn()
+        e1.record(stream)
         torch.cuda.synchronize()
+        prof = ctx.profile_read() if profile else None
+        if profile:
+            ctx.profile(False)
         barrier()
         ms = e0.elapsed_time(e1) / args.steps
         if world > 1:
@@ -203,30 +247,62 @@ def run_ours(args):
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        return ms, ctx.kernel_launches - l0
+        return ms, ctx.kernel_launches - l0, prof
 
     with ClockSampler(local) as clk:
-        ms, launches = timed(A.PODE_DEVICE)
-    ms_e2e, _ = timed(A.PODE_HOST)
+        ms, launches, prof = timed(solve_device, profile=True)
+    ms_e2e, _, _ = timed(solve_public)
     value = world * n / (ms * 1e-3)
     e2e = world * n / (ms_e2e * 1e-3)
-    d2h = sum(t.numel() * 8 for t in out_host)
+    d2h = n1 * (D + D * D + d + d * d) * 8
     h2d = n1 * 8
     if rank != 0:
         return
+
+    # roofline of the dominant kernel (largest share of the timed region)
+    hbm, hbm_src, fp64, fp64_src = peaks()
+    model = kernel_model(D, d)
+    total_ms = sum(v[1] for v in prof.values())
+    dom = max(prof.items(), key=lambda kv: kv[1][1])
+    name, (cnt, kms) = dom
+    avg_s = kms / cnt * 1e-3
+    roof = {"kernel": name, "share_of_step": kms / total_ms if total_ms else None}
+    if name in model:
+        flops, bytes_ = model[name]
+        t_fp64 = flops * n / (fp64 * 1e12)
+        t_hbm = bytes_ * n / (hbm * 1e9)
+        traffic = None
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+            traffic = tr.get(f"{name}@2^{args.log2n}")
+        except Exception:
+            pass
+        if t_fp64 >= t_hbm:
+            achieved = flops * n / avg_s / 1e12
+            roof.update({"bound": "fp64", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+                         "frac": achieved / fp64, "peak_source": fp64_src})
+        else:
+            achieved = bytes_ * n / avg_s / 1e9
+            roof.update({"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "peak_source": hbm_src})
+        roof.update({"traffic": traffic, "algorithmic_flops_per_launch": flops * n,
+                     "algorithmic_bytes_per_launch": bytes_ * n, "avg_launch_ms": avg_s * 1e3})
+    kernels = {k: {"launches": c, "ms_per_step": t / args.steps} for k, (c, t) in sorted(prof.items())}
     line = {"metric": METRIC, "value": value, "unit": "time-steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{prob.name} d={d} IWP(q={nu}) D={D}, N=2^{args.log2n} uniform steps, "
-                                   "full IEKS to convergence", "N": n, "iterations": iters,
-                       "step_iterations_per_s": value * iters, "parallelism": f"replicas x{world}",
-                       "l2": "working set > L2 (126 MB)"},
-            "clocks": clk.summary(), "gpu_launches": int(launches),
-            "e2e": {"value": e2e, "unit": "time-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}}
+                                   "IEKS to the reference stopping rule", "N": n, "iterations": iters,
+                       "converged": converged, "step_iterations_per_s": value * iters / world,
+                       "parallelism": f"replicas x{world}", "l2": "working set > L2 (126 MB) per solve"},
+            "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof,
+            "e2e": {"value": e2e, "unit": "time-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "kernels": kernels}
     if not args.no_cpu_baseline:
-        v, t, it = cpu_reference(args, args.problem, nu, CPU_SAMPLE_N, 1, 0, 0)
-        line["cpu_baseline"] = {"value": v, "unit": "time-steps/s", "cores": 1, "kind": "port",
-                                "sample": f"seq_ieks (single thread) full solve at N={CPU_SAMPLE_N}, {it} iterations"}
+        t, it = cpu_solve(args.problem, nu, CPU_SAMPLE_N, 0)
+        line["cpu_baseline"] = {"value": CPU_SAMPLE_N / t, "unit": "time-steps/s", "cores": 1, "kind": "port",
+                                "sample": f"seq_ieks (single thread) full solve at N={CPU_SAMPLE_N}, "
+                                          f"{it} iterations"}
     print(json.dumps(line), flush=True)
 
 

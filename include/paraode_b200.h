@@ -67,6 +67,12 @@ int32_t pode_max_state_dim(void);
 int64_t pode_kernel_launches(const pode_context* ctx);
 /* The CUDA stream (cudaStream_t) the context launches on. */
 void* pode_context_stream(pode_context* ctx);
+/* Per-kernel CUDA-event timing on the context stream (instrumentation):
+ * pode_profile(ctx, 1) clears and starts recording, pode_profile(ctx, 0)
+ * stops; pode_profile_read writes "kernel launches total_ms" lines into buf
+ * and returns the full text length (-1 on error). */
+int pode_profile(pode_context* ctx, int32_t enable);
+int64_t pode_profile_read(pode_context* ctx, char* buf, int64_t size);
 
 /* ------------------------------------------------------------- elements */
 /* FilteringElement arrays (proj/include/paraode/parallel.hpp:20-26):

@@ -67,6 +67,8 @@ SYMBOLS = {
     "pode_max_state_dim": (C.c_int32, []),
     "pode_kernel_launches": (C.c_int64, [C.c_void_p]),
     "pode_context_stream": (C.c_void_p, [C.c_void_p]),
+    "pode_profile": (C.c_int, [C.c_void_p, C.c_int32]),
+    "pode_profile_read": (C.c_int64, [C.c_void_p, C.c_char_p, C.c_int64]),
     "pode_make_filtering_elements": (C.c_int, [C.c_void_p, C.POINTER(Chain), C.c_int32,
                                                FilteringElements, C.POINTER(Status)]),
     "pode_combine_filtering": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, FilteringElements,

@@ -90,6 +90,21 @@ class Context:
     def stream(self) -> int:
         return int(self._lib.pode_context_stream(self._h) or 0)
 
+    def profile(self, enable: bool):
+        """Start (clear) / stop per-kernel CUDA-event timing on the context stream."""
+        self._lib.pode_profile(self._h, int(enable))
+
+    def profile_read(self):
+        """{kernel: (launches, total_ms)} recorded since profile(True)."""
+        n = self._lib.pode_profile_read(self._h, None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        self._lib.pode_profile_read(self._h, buf, int(n) + 1)
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, ms = line.rsplit(" ", 2)
+            out[name] = (int(cnt), float(ms))
+        return out
+
     def close(self):
         if self._h:
             self._lib.pode_context_destroy(self._h)

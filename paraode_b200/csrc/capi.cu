@@ -52,6 +52,7 @@ unsigned long long fetch_error(pode_context* ctx) {
                              ctx->stream),
              "fetch error word");
   cuda_check(cudaStreamSynchronize(ctx->stream), "stream sync");
+  prof_mark(ctx);
   return *ctx->h_err;
 }
 
@@ -277,11 +278,51 @@ void pode_context_destroy(pode_context* ctx) {
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
+  for (cudaEvent_t e : ctx->prof_pool) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
 
 int32_t pode_max_state_dim(void) { return kMaxD; }
+
+int pode_profile(pode_context* ctx, int32_t enable) {
+  if (ctx == nullptr) return PODE_ERR_INVALID_INPUT;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->prof.clear();
+  ctx->prof_used = 0;
+  ctx->prof_on = enable != 0;
+  if (ctx->prof_on) prof_mark(ctx);
+  return PODE_OK;
+}
+
+int64_t pode_profile_read(pode_context* ctx, char* buf, int64_t size) {
+  if (ctx == nullptr) return -1;
+  cudaSetDevice(ctx->device);
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return -1;
+  std::map<std::string, std::pair<int64_t, double>> agg;
+  for (size_t i = 1; i < ctx->prof.size(); ++i) {
+    if (ctx->prof[i].name == nullptr) continue;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->prof[i - 1].ev, ctx->prof[i].ev) != cudaSuccess) continue;
+    auto& a = agg[ctx->prof[i].name];
+    a.first += 1;
+    a.second += ms;
+  }
+  std::string out;
+  for (const auto& kv : agg) {
+    char line[256];
+    std::snprintf(line, sizeof(line), "%s %lld %.6f\n", kv.first.c_str(), static_cast<long long>(kv.second.first),
+                  kv.second.second);
+    out += line;
+  }
+  if (buf != nullptr && size > 0) {
+    const size_t n = std::min<size_t>(out.size(), size_t(size - 1));
+    std::memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return int64_t(out.size());
+}
 
 int64_t pode_kernel_launches(const pode_context* ctx) { return ctx ? ctx->launches : 0; }
 

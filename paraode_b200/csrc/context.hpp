@@ -10,6 +10,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/paraode_b200.h"
 
@@ -62,6 +63,14 @@ struct Workspace {
 
 }  // namespace pode
 
+// Per-launch CUDA-event timing (pode_profile): an event is recorded on the
+// context stream after every launch and at every host synchronisation point;
+// a kernel's duration is the interval since the previous record.
+struct ProfRec {
+  const char* name;  // nullptr for a synchronisation marker
+  cudaEvent_t ev;
+};
+
 struct pode_context {
   int device = 0;
   int sm_count = 148;
@@ -71,14 +80,38 @@ struct pode_context {
   unsigned long long* h_err = nullptr;  // pinned mirror
   double* h_scalars = nullptr;          // pinned scalars (reductions)
   int64_t launches = 0;
+  bool prof_on = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> prof_pool;
+  size_t prof_used = 0;
 };
 
 namespace pode {
 
+inline cudaEvent_t prof_event(pode_context* ctx) {
+  if (ctx->prof_used == ctx->prof_pool.size()) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "profile event");
+    ctx->prof_pool.push_back(e);
+  }
+  return ctx->prof_pool[ctx->prof_used++];
+}
+
+inline void prof_record(pode_context* ctx, const char* name) {
+  if (!ctx->prof_on) return;
+  cudaEvent_t e = prof_event(ctx);
+  cuda_check(cudaEventRecord(e, ctx->stream), "profile record");
+  ctx->prof.push_back({name, e});
+}
+
 inline void note_launch(pode_context* ctx, const char* what) {
   ctx->launches += 1;
   cuda_check(cudaGetLastError(), what);
+  prof_record(ctx, what);
 }
+
+// After a host synchronisation: the next launch's interval starts here.
+inline void prof_mark(pode_context* ctx) { prof_record(ctx, nullptr); }
 
 // Resets the device error word (before a stage) / reads it back (after).
 void reset_error(pode_context* ctx);

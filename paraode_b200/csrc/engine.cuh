@@ -100,6 +100,8 @@ template <int D>
 struct FOps {
   using El = FEl<D>;
   using Arr = FEd;
+  static constexpr const char* kReduce = "scan_f_reduce";
+  static constexpr const char* kDown = "scan_f_down";
   __device__ static El load(const Arr& x, int64_t i, int r, bool ok) {
     El e;
     e.a = ld_row<D>(x.a, i, r, ok);
@@ -137,6 +139,8 @@ template <int D>
 struct SOps {
   using El = SEl<D>;
   using Arr = SEd;
+  static constexpr const char* kReduce = "scan_s_reduce";
+  static constexpr const char* kDown = "scan_s_down";
   __device__ static El load(const Arr& x, int64_t i, int r, bool ok) {
     El e;
     e.e = ld_row<D>(x.e, i, r, ok);
@@ -173,6 +177,8 @@ struct MOps {
     double g;
   };
   using Arr = SEd;  // l unused
+  static constexpr const char* kReduce = "scan_m_reduce";
+  static constexpr const char* kDown = "scan_m_down";
   __device__ static El load(const Arr& x, int64_t i, int r, bool ok) {
     El e;
     e.e = ld_row<D>(x.e, i, r, ok);
@@ -375,7 +381,7 @@ struct Engine {
     if (n <= L) {
       k_scan_down<D, Op, kReverse><<<1, kThreads, smem_bytes<D>(), ctx->stream>>>(in, n, static_cast<int>(n),
                                                                                    in, 0, out, err);
-      note_launch(ctx, "scan_down");
+      note_launch(ctx, Op::kDown);
       t.combines += n - 1;
       t.depth += n - 1;
       return;
@@ -383,13 +389,13 @@ struct Engine {
     const int64_t nc = (n + L - 1) / L;
     typename Op::Arr agg = alloc<Op>(ctx, "scan_agg_" + std::to_string(level), nc);
     k_scan_reduce<D, Op><<<blocks_for<D>(nc), kThreads, smem_bytes<D>(), ctx->stream>>>(in, n, L, agg, err);
-    note_launch(ctx, "scan_reduce");
+    note_launch(ctx, Op::kReduce);
     t.combines += n - nc;
     t.depth += L - 1;
     scan_rec<Op, kReverse>(ctx, agg, agg, nc, level + 1, t);
     k_scan_down<D, Op, kReverse><<<blocks_for<D>(nc), kThreads, smem_bytes<D>(), ctx->stream>>>(in, n, L, agg,
                                                                                                 nc, out, err);
-    note_launch(ctx, "scan_down");
+    note_launch(ctx, Op::kDown);
     t.combines += n - 1;
     t.depth += L;
   }

@@ -133,11 +133,13 @@ struct FastEngine {
         tf = Engine<D>::scan_filtering(ctx, nc, agg, agg, false);
       if (lanes) {
         lane::k_lane_fwd_down<D, d><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, agg, elems, bagg);
-        note_launch(ctx, "lane_fwd_down");
+        note_launch(ctx, "fast_fwd_down");
         lane::k_lane_bfold<D><<<lblocks, lane::kLaneThreads, 0, st>>>(elems, N, L, nc, bagg);
-      } else
+        note_launch(ctx, "fast_bwd_fold");
+      } else {
         k_fast_fwd_down<D, d><<<blocks, kThreads, sm, st>>>(a, cst, agg, elems, bagg);
-      note_launch(ctx, "fast_fwd_down");
+        note_launch(ctx, "fast_fwd_down");
+      }
       if (lane_scans())
         lane::LaneScan<D, lane::LMOps<D>, true>::run(ctx, bagg, bagg, nc, 0, scan_fanin(), tr);
       else
