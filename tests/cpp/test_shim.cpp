@@ -1,0 +1,135 @@
+// Reads like the reference's own tests (proj/tests/test_ieks.cpp,
+// test_parallel.cpp) but runs the reference-facing C++ shim
+// (include/paraode/paraode_b200.hpp) on the B200.  A tiny dense type stands
+// in for Eigen::MatrixXd / VectorXd (the shim is templated on them).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "paraode/paraode_b200.hpp"
+
+struct Mat {
+  int r = 0, c = 0;
+  std::vector<double> v;
+  Mat() = default;
+  Mat(int rows, int cols) : r(rows), c(cols), v(size_t(rows) * cols, 0.0) {}
+  int rows() const { return r; }
+  int cols() const { return c; }
+  double& operator()(int i, int j) { return v[size_t(i) * c + j]; }
+  double operator()(int i, int j) const { return v[size_t(i) * c + j]; }
+};
+struct Vec {
+  std::vector<double> v;
+  Vec() = default;
+  explicit Vec(int n) : v(size_t(n), 0.0) {}
+  int size() const { return int(v.size()); }
+  double& operator[](int i) { return v[size_t(i)]; }
+  double operator[](int i) const { return v[size_t(i)]; }
+};
+struct Gauss {
+  Vec mean;
+  Mat cov_sqrt;
+};
+struct Trans {
+  Mat phi, q_sqrt;
+};
+struct Obs {
+  Mat h;
+  Vec offset;
+  Mat r_sqrt;
+};
+
+static int failures = 0;
+#define CHECK(cond)                                                    \
+  do {                                                                 \
+    if (!(cond)) {                                                     \
+      std::fprintf(stderr, "CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+      ++failures;                                                      \
+    }                                                                  \
+  } while (0)
+
+namespace pb = paraode::b200;
+
+int main() {
+  pb::Device gpu(0);
+
+  // logistic, nu = 2, N = 30 (test_ieks.cpp:271-282, acceptance.cpp:167-179)
+  {
+    pb::Problem p;  // logistic defaults
+    std::vector<double> grid(31);
+    for (int n = 0; n <= 30; ++n) grid[n] = 10.0 * n / 30.0;
+    auto rep = pb::para_ieks<Mat, Vec>(p, pb::IwpPrior{2, 1, 1.0}, grid, pb::IeksConfig{}, gpu);
+    CHECK(rep.converged);
+    const double want = 0.01 / (0.01 + 0.99 * std::exp(-10.0));
+    CHECK(std::fabs(rep.solution_means.back()[0] - want) <= 1e-4);
+    CHECK(rep.sigma_hat > 0.0);
+    CHECK(rep.objective_trace.size() == size_t(rep.iterations));
+    double acc = 0.0;
+    for (int n = 0; n <= 30; ++n) {
+      const double e = rep.solution_means[n][0] - 0.01 / (0.01 + 0.99 * std::exp(-grid[n]));
+      acc += e * e;
+    }
+    CHECK(std::sqrt(acc / 31.0) <= 2.1e-6);  // frozen gate; reference measured 1.374e-6
+  }
+
+  // errors map to the reference's exception types (test_ieks.cpp:369-388)
+  {
+    pb::Problem p;
+    pb::IeksConfig cfg;
+    cfg.max_iterations = 0;
+    bool threw = false;
+    try {
+      pb::para_ieks<Mat, Vec>(p, pb::IwpPrior{2, 1, 1.0}, {0.0, 1.0}, cfg, gpu);
+    } catch (const pb::InvalidInputError&) {
+      threw = true;
+    }
+    CHECK(threw);
+    threw = false;
+    try {
+      pb::para_ieks<Mat, Vec>(p, pb::IwpPrior{2, 2, 1.0}, {0.0, 1.0}, pb::IeksConfig{}, gpu);
+    } catch (const pb::DimensionError&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+
+  // para_rts on a scalar random-walk chain against the closed form
+  {
+    const int N = 50;
+    Gauss init{Vec(1), Mat(1, 1)};
+    init.mean[0] = 0.0;
+    init.cov_sqrt(0, 0) = 1.0;
+    std::vector<Trans> tr(N);
+    std::vector<Obs> ob(N);
+    for (int n = 0; n < N; ++n) {
+      tr[n].phi = Mat(1, 1);
+      tr[n].phi(0, 0) = 1.0;
+      tr[n].q_sqrt = Mat(1, 1);
+      tr[n].q_sqrt(0, 0) = 0.3;
+      ob[n].h = Mat(1, 1);
+      ob[n].h(0, 0) = 1.0;
+      ob[n].offset = Vec(1);
+      ob[n].offset[0] = std::sin(0.1 * n);
+      ob[n].r_sqrt = Mat(1, 1);
+      ob[n].r_sqrt(0, 0) = 0.5;
+    }
+    auto res = pb::para_rts<Mat, Vec>(init, tr, ob, gpu);
+    // scalar sequential Kalman filter
+    double m = 0.0, P = 1.0, worst = 0.0;
+    for (int n = 0; n < N; ++n) {
+      P += 0.09;
+      const double k = P / (P + 0.25);
+      m += k * (ob[n].offset[0] - m);
+      P *= (1 - k);
+      worst = std::fmax(worst, std::fabs(res.filtered[n + 1].mean[0] - m));
+      worst = std::fmax(worst, std::fabs(res.filtered[n + 1].cov_sqrt(0, 0) * res.filtered[n + 1].cov_sqrt(0, 0) - P));
+    }
+    CHECK(worst <= 1e-12);
+    CHECK(res.smoothed.size() == size_t(N + 1));
+    CHECK(res.stats.combine_invocations > 0);
+  }
+
+  std::printf("%s (%d failures)\n", failures ? "FAIL" : "PASS", failures);
+  return failures ? 1 : 0;
+}
