@@ -356,6 +356,99 @@ __global__ void __launch_bounds__(kThreads) k_scan_down(typename Op::Arr x, int6
   if (okc && g.r == 0 && bad) raise_error(err, lo, kErrSingular);
 }
 
+// --------------------------------------------- Gaussian-carry ⊗_f scan ---
+// Reduce that also keeps every chunk-local inclusive prefix (loc), so the
+// down-sweep is ONE combine deep: out[k] = carry ⊗ loc[k], independent k.
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_scan_reduce_loc(FEd x, int64_t n, int L, FEd loc, FEd agg,
+                                                              DevError* err) {
+  extern __shared__ double smem[];
+  const Grp<D> g = make_group<D>(smem);
+  const int64_t c = group_index<D>(g);
+  const int64_t lo = c * L;
+  const int64_t hi = min(n, lo + L);
+  const bool okc = g.real() && lo < n;
+  FEl<D> acc = FOps<D>::load(x, lo, g.r, okc);
+  FOps<D>::store(loc, lo, g.r, okc, acc);
+  bool bad = false;
+  for (int t = 1; t < L; ++t) {
+    const int64_t k = lo + t;
+    const bool ok = okc && k < hi;
+    const FEl<D> e = FOps<D>::load(x, k, g.r, ok);
+    FEl<D> tmp;
+    const bool good = combine_filtering<D>(g, acc, e, tmp);
+    bad |= ok && !good;
+    acc = FOps<D>::select(ok, tmp, acc);
+    FOps<D>::store(loc, k, g.r, ok, acc);
+  }
+  if (okc && g.r == 0 && bad) raise_error(err, lo, kErrSingular);
+  FOps<D>::store(agg, c, g.r, okc, acc);
+}
+
+// out[k] (b, C only) = carry[k / L - 1] ⊗ loc[k]; chunk 0 copies loc.
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_scan_down_gauss(FEd loc, int64_t n, int L, FEd carry, FEd out,
+                                                              DevError* err) {
+  extern __shared__ double smem[];
+  const Grp<D> g = make_group<D>(smem);
+  const int64_t k = group_index<D>(g);
+  const bool ok = g.real() && k < n;
+  const int64_t c = k / L;
+  const bool first = c == 0;
+  const FEl<D> e = FOps<D>::load(loc, k, g.r, ok);
+  const double bi = ld_ent<D>(carry.b, c - 1, g.r, ok && !first);
+  const Rw<D> ci = ld_row<D>(carry.c, c - 1, g.r, ok && !first);
+  double bo;
+  Rw<D> co;
+  const bool good = combine_gauss<D>(g, bi, ci, e, bo, co);
+  if (ok && !first && g.r == 0 && !good) raise_error(err, k, kErrSingular);
+  st_ent<D>(out.b, k, g.r, ok, first ? e.b : bo);
+  st_row<D>(out.c, k, g.r, ok, first ? e.c : co);
+}
+
+// ------------------------------------- reverse mean-only scan (E = 0 tail) ---
+// Chunk-local suffixes loc[k] = e_k ⊗ .. ⊗ e_{hi-1} (⊗_s on (E, g)) and the
+// chunk aggregate; the sequence ends in the terminal element (E = 0), so
+// every global suffix is a Gaussian mean and the down-sweep is one matvec.
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_mscan_reduce_loc(SEd x, int64_t n, int L, SEd loc, SEd agg) {
+  extern __shared__ double smem[];
+  const Grp<D> g = make_group<D>(smem);
+  const int64_t c = group_index<D>(g);
+  const int64_t lo = c * L;
+  const int64_t hi = min(n, lo + L);
+  const bool okc = g.real() && lo < n;
+  typename MOps<D>::El acc = MOps<D>::load(x, hi - 1, g.r, okc);
+  MOps<D>::store(loc, hi - 1, g.r, okc, acc);
+  for (int t = 1; t < L; ++t) {
+    const int64_t k = hi - 1 - t;
+    const bool ok = okc && k >= lo;
+    const typename MOps<D>::El e = MOps<D>::load(x, k, g.r, ok);
+    typename MOps<D>::El tmp;
+    MOps<D>::combine(g, e, acc, tmp);
+    acc = MOps<D>::select(ok, tmp, acc);
+    MOps<D>::store(loc, k, g.r, ok, acc);
+  }
+  MOps<D>::store(agg, c, g.r, okc, acc);
+}
+
+// out.g[k] = loc[k] ⊗ (0, g_carry) = E_loc g_carry + g_loc, carry = the
+// suffix of the next chunk (the last chunk copies loc).
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_mscan_down(SEd loc, int64_t n, int L, int64_t nchunks, SEd carry,
+                                                         SEd out) {
+  extern __shared__ double smem[];
+  const Grp<D> g = make_group<D>(smem);
+  const int64_t k = group_index<D>(g);
+  const bool ok = g.real() && k < n;
+  const int64_t c = k / L;
+  const bool last = c >= nchunks - 1;
+  const typename MOps<D>::El e = MOps<D>::load(loc, k, g.r, ok);
+  const double gc = ld_ent<D>(carry.g, c + 1, g.r, ok && !last);
+  const double go = matvec(g, e.e, gc) + e.g;
+  st_ent<D>(out.g, k, g.r, ok, last ? e.g : go);
+}
+
 // ------------------------------------------------------------- engine ---
 template <int D>
 struct Engine {
@@ -417,6 +510,93 @@ struct Engine {
     cudaFuncSetAttribute(k_scan_down<D, SOps<D>, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(k_scan_reduce<D, MOps<D>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(k_scan_down<D, MOps<D>, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  }
+
+  // Inclusive ⊗_f scan of a sequence whose first element is Gaussian
+  // (A = eta = J = 0): every prefix is Gaussian, so only its (b, C) are
+  // produced (into out.b / out.c).  k-ary tree with local prefixes: depth
+  // (L-1) full combines per level up, ONE Gaussian-carry combine per level
+  // down.
+  static void scan_gauss_rec(pode_context* ctx, FEd in, FEd out, int64_t n, int level, int L, ScanTally& t) {
+    DevError* err = reinterpret_cast<DevError*>(ctx->d_err);
+    const size_t sm = smem_bytes<D>();
+    FEd loc = alloc<FOps<D>>(ctx, "gscan_loc_" + std::to_string(level), n);
+    if (n <= L) {
+      k_scan_reduce_loc<D><<<1, kThreads, sm, ctx->stream>>>(in, n, static_cast<int>(n), loc, loc, err);
+      note_launch(ctx, "scan_g_reduce");
+      t.combines += n - 1;
+      t.depth += n - 1;
+      cuda_check(cudaMemcpyAsync(out.b, loc.b, sizeof(double) * D * n, cudaMemcpyDeviceToDevice, ctx->stream),
+                 "gscan copy");
+      cuda_check(cudaMemcpyAsync(out.c, loc.c, sizeof(double) * D * D * n, cudaMemcpyDeviceToDevice, ctx->stream),
+                 "gscan copy");
+      return;
+    }
+    const int64_t nc = (n + L - 1) / L;
+    FEd agg = alloc<FOps<D>>(ctx, "gscan_agg_" + std::to_string(level), nc);
+    k_scan_reduce_loc<D><<<blocks_for<D>(nc), kThreads, sm, ctx->stream>>>(in, n, L, loc, agg, err);
+    note_launch(ctx, "scan_g_reduce");
+    t.combines += n - nc;
+    t.depth += L - 1;
+    scan_gauss_rec(ctx, agg, agg, nc, level + 1, L, t);
+    k_scan_down_gauss<D><<<blocks_for<D>(n), kThreads, sm, ctx->stream>>>(loc, n, L, agg, out, err);
+    note_launch(ctx, "scan_g_down");
+    t.combines += n - std::min<int64_t>(n, L);
+    t.depth += 1;
+  }
+
+  static ScanTally scan_filtering_gauss(pode_context* ctx, int64_t n, FEd in, FEd out, int L) {
+    set_smem();
+    static bool attr = false;
+    if (!attr) {
+      attr = true;
+      const int bytes = static_cast<int>(smem_bytes<D>());
+      cudaFuncSetAttribute(k_scan_reduce_loc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      cudaFuncSetAttribute(k_scan_down_gauss<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    }
+    ScanTally t;
+    if (n >= 1) scan_gauss_rec(ctx, in, out, n, 0, L, t);
+    return t;
+  }
+
+  // Reverse inclusive scan of mean-only elements ending in the terminal
+  // element (E = 0): only the suffix means (out.g) are produced.
+  static void mscan_rec(pode_context* ctx, SEd in, SEd out, int64_t n, int level, int L, ScanTally& t) {
+    const size_t sm = smem_bytes<D>();
+    SEd loc = alloc<SOps<D>>(ctx, "mscan_loc_" + std::to_string(level), n);
+    if (n <= L) {
+      k_mscan_reduce_loc<D><<<1, kThreads, sm, ctx->stream>>>(in, n, static_cast<int>(n), loc, loc);
+      note_launch(ctx, "scan_m_reduce");
+      t.combines += n - 1;
+      t.depth += n - 1;
+      cuda_check(cudaMemcpyAsync(out.g, loc.g, sizeof(double) * D * n, cudaMemcpyDeviceToDevice, ctx->stream),
+                 "mscan copy");
+      return;
+    }
+    const int64_t nc = (n + L - 1) / L;
+    SEd agg = alloc<SOps<D>>(ctx, "mscan_agg_" + std::to_string(level), nc);
+    k_mscan_reduce_loc<D><<<blocks_for<D>(nc), kThreads, sm, ctx->stream>>>(in, n, L, loc, agg);
+    note_launch(ctx, "scan_m_reduce");
+    t.combines += n - nc;
+    t.depth += L - 1;
+    mscan_rec(ctx, agg, agg, nc, level + 1, L, t);
+    k_mscan_down<D><<<blocks_for<D>(n), kThreads, sm, ctx->stream>>>(loc, n, L, nc, agg, out);
+    note_launch(ctx, "scan_m_down");
+    t.combines += n - std::min<int64_t>(n, L);
+    t.depth += 1;
+  }
+
+  static ScanTally scan_means_terminal(pode_context* ctx, int64_t n, SEd io, int L) {
+    static bool attr = false;
+    if (!attr) {
+      attr = true;
+      const int bytes = static_cast<int>(smem_bytes<D>());
+      cudaFuncSetAttribute(k_mscan_reduce_loc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      cudaFuncSetAttribute(k_mscan_down<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    }
+    ScanTally t;
+    if (n >= 1) mscan_rec(ctx, io, io, n, 0, L, t);
+    return t;
   }
 
   // Reverse inclusive scan of mean-only smoothing elements.

@@ -78,10 +78,14 @@ struct FastEngine {
     double* eta_a = ws.arr<double>("ieks_eta_a", n1 * D);
     double* eta_b = ws.arr<double>("ieks_eta_b", n1 * D);
     FEd agg = Engine<D>::template alloc<FOps<D>>(ctx, "fast_agg", nc);
-    SEd elems;
+    SEd elems;  // element-major (group passes)
+    lane::ElemSoA soa;  // chunk-interleaved (lane passes)
     {
-      double* base = ws.arr<double>("fast_elems", size_t(n1) * (D * D + D));
-      elems = SEd{base, base + size_t(n1) * D * D, nullptr};
+      const size_t padded = size_t(nc) * L;
+      const size_t n_el = std::max<size_t>(size_t(n1), padded + 1);
+      double* base = ws.arr<double>("fast_elems", n_el * (D * D + D) + D);
+      elems = SEd{base, base + n_el * D * D, nullptr};
+      soa = lane::ElemSoA{base, base + padded * D * D, base + n_el * (D * D + D), nc, L};
     }
     SEd bagg;
     {
@@ -106,7 +110,7 @@ struct FastEngine {
     // objective of the constant start (ieks.cpp:147-148)
     a.eta = eta_a;
     if (lanes)
-      lane::k_lane_bwd_down<D, d, true><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, elems, bagg, eta_a, eta_b,
+      lane::k_lane_bwd_down<D, d, true><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, soa, bagg, eta_a, eta_b,
                                                                                part);
     else
       k_fast_bwd_down<D, d, true><<<blocks, kThreads, sm, st>>>(a, cst, elems, bagg, eta_a, eta_b, part);
@@ -130,11 +134,11 @@ struct FastEngine {
       if (lane_scans())
         lane::LaneScan<D, lane::LFOps<D>, false>::run(ctx, agg, agg, nc, 0, scan_fanin(), tf);
       else
-        tf = Engine<D>::scan_filtering(ctx, nc, agg, agg, false);
+        tf = Engine<D>::scan_filtering_gauss(ctx, nc, agg, agg, scan_fanin());
       if (lanes) {
-        lane::k_lane_fwd_down<D, d><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, agg, elems, bagg);
+        lane::k_lane_fwd_down<D, d><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, agg, soa);
         note_launch(ctx, "fast_fwd_down");
-        lane::k_lane_bfold<D><<<lblocks, lane::kLaneThreads, 0, st>>>(elems, N, L, nc, bagg);
+        lane::k_lane_bfold<D><<<lblocks, lane::kLaneThreads, 0, st>>>(soa, N, L, nc, bagg);
         note_launch(ctx, "fast_bwd_fold");
       } else {
         k_fast_fwd_down<D, d><<<blocks, kThreads, sm, st>>>(a, cst, agg, elems, bagg);
@@ -143,9 +147,9 @@ struct FastEngine {
       if (lane_scans())
         lane::LaneScan<D, lane::LMOps<D>, true>::run(ctx, bagg, bagg, nc, 0, scan_fanin(), tr);
       else
-        tr = Engine<D>::scan_means_reverse(ctx, nc, bagg);
+        tr = Engine<D>::scan_means_terminal(ctx, nc, bagg, scan_fanin());
       if (lanes)
-        lane::k_lane_bwd_down<D, d, false><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, elems, bagg, eta_a,
+        lane::k_lane_bwd_down<D, d, false><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, soa, bagg, eta_a,
                                                                                   eta_b, part);
       else
         k_fast_bwd_down<D, d, false><<<blocks, kThreads, sm, st>>>(a, cst, elems, bagg, eta_a, eta_b, part);

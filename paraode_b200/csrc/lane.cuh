@@ -303,6 +303,41 @@ struct Model {
   }
 };
 
+// Per-node smoothing elements (E_n, g_n) in a chunk-interleaved
+// structure-of-arrays layout: entry x of node n = c L + t (chunk c, local
+// step t) lives at (t * X + x) * nc + c, X = D*D for E and D for g, so the
+// 32 lanes of a warp (32 consecutive chunks) touch 32 consecutive doubles on
+// every access.  The terminal node N (E = 0, g = m_f(N)) is kept in `term`.
+struct ElemSoA {
+  double* e;
+  double* g;
+  double* term;
+  int64_t nc;
+  int L;
+};
+
+template <int D>
+__device__ __forceinline__ void soa_st(const ElemSoA& s, int64_t c, int64_t t, const double (&E)[D][D],
+                                       const double (&g)[D]) {
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) s.e[((t * D + r) * D + j) * s.nc + c] = E[r][j];
+    s.g[(t * D + r) * s.nc + c] = g[r];
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void soa_ld(const ElemSoA& s, int64_t c, int64_t t, double (&E)[D][D],
+                                       double (&g)[D]) {
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) E[r][j] = s.e[((t * D + r) * D + j) * s.nc + c];
+    g[r] = s.g[(t * D + r) * s.nc + c];
+  }
+}
+
 template <int D>
 __device__ __forceinline__ void ld_mat(const double* p, double (&m)[D][D]) {
 #pragma unroll
@@ -442,10 +477,10 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(FastArgs a, Fa
 // ------------------------------------------------------------- pass C ---
 // One thread per chunk: square-root Kalman filter from the chunk's incoming
 // filtered marginal; smoothing elements E_n, g_n (parallel.cpp:112-135) of
-// every node, and the chunk's backward aggregate (E, g).
+// every node (chunk-interleaved layout, ElemSoA).
 template <int D, int d>
 __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, FastConst<D> cst, FEd prefix,
-                                                                SEd elems, SEd bagg) {
+                                                                ElemSoA elems) {
   using M = Model<D, d>;
   constexpr int B = M::B;
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -529,9 +564,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
       for (int j = 0; j < D; ++j) acc = fma(E[r][j], mm[j], acc);
       gk[r] = m[r] - acc;
     }
-    st_mat<D>(elems.e + k * D * D, E);
-#pragma unroll
-    for (int r = 0; r < D; ++r) elems.g[k * D + r] = gk[r];
+    soa_st<D>(elems, c, k - s, E, gk);
     // measurement update at node k+1
     const typename M::Lin lin = M::linearize(a.prob, a.eta + (k + 1) * D, a.ek0);
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
@@ -556,15 +589,10 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
   }
   if (e == a.N) {  // terminal node N: E = 0, g = m_f(N) (parallel.cpp:137-144)
 #pragma unroll
-    for (int r = 0; r < D; ++r) {
-#pragma unroll
-      for (int x = 0; x < D; ++x) elems.e[(a.N * D + r) * D + x] = 0.0;
-      elems.g[a.N * D + r] = m[r];
-    }
+    for (int r = 0; r < D; ++r) elems.term[r] = m[r];
   }
   if (bad_lin >= 0) raise_error(a.err, bad_lin, kErrLinearization);
   if (bad_sing) raise_error(a.err, s, kErrSingular);
-  (void)bagg;
 }
 
 // Pass C2: one thread per chunk folds the chunk's smoothing elements in time
@@ -572,21 +600,28 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
 // (⊗_s on means, parallel.cpp:146-156); the last chunk includes the
 // terminal node N, so its aggregate has E = 0.
 template <int D>
-__global__ void __launch_bounds__(kLaneThreads) k_lane_bfold(SEd elems, int64_t N, int L, int64_t nchunks,
+__global__ void __launch_bounds__(kLaneThreads) k_lane_bfold(ElemSoA elems, int64_t N, int L, int64_t nchunks,
                                                              SEd bagg) {
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (c >= nchunks) return;
   const int64_t s = c * L;
-  const int64_t e = (c == nchunks - 1) ? N + 1 : min(N, s + L);
+  const int64_t e = min(N, s + L);
+  const bool last = c == nchunks - 1;
   double Eg[D][D], gg[D];
-  ld_mat<D>(elems.e + s * D * D, Eg);
-#pragma unroll
-  for (int r = 0; r < D; ++r) gg[r] = elems.g[s * D + r];
-  for (int64_t k = s + 1; k < e; ++k) {
+  soa_ld<D>(elems, c, 0, Eg, gg);
+  for (int64_t k = s + 1; k <= e; ++k) {
     double E[D][D], gk[D];
-    ld_mat<D>(elems.e + k * D * D, E);
+    if (k < e) {
+      soa_ld<D>(elems, c, k - s, E, gk);
+    } else {  // node e: only the terminal node N belongs to this chunk
+      if (!last) break;
 #pragma unroll
-    for (int r = 0; r < D; ++r) gk[r] = elems.g[k * D + r];
+      for (int r = 0; r < D; ++r) {
+        gk[r] = elems.term[r];
+#pragma unroll
+        for (int j = 0; j < D; ++j) E[r][j] = 0.0;
+      }
+    }
 #pragma unroll
     for (int r = 0; r < D; ++r) {
       double o[D], og = gg[r];
@@ -613,7 +648,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_bfold(SEd elems, int64_t 
 // from the chunk's incoming smoothed mean; new trajectory (original
 // coordinates) and per-chunk objective / stopping partials.
 template <int D, int d, bool kInitial>
-__global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, FastConst<D> cst, SEd elems,
+__global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, FastConst<D> cst, ElemSoA elems,
                                                                 SEd suffix, const double* eta_old,
                                                                 double* eta_new, double* part) {
   using M = Model<D, d>;
@@ -636,7 +671,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, Fast
         eta_e = eta_old[e * D + r];
         mu[r] = 0.0;
       } else {
-        mu[r] = last ? elems.g[a.N * D + r] : suffix.g[(c + 1) * D + r];
+        mu[r] = last ? elems.term[r] : suffix.g[(c + 1) * D + r];
         eta_e = te[r % B] * mu[r];
       }
       if (last) {
@@ -657,11 +692,11 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, Fast
 #pragma unroll
         for (int r = 0; r < D; ++r) etak[r] = eta_old[k * D + r];
       } else {
-        double E[D][D], nm[D];
-        ld_mat<D>(elems.e + k * D * D, E);
+        double E[D][D], gk[D], nm[D];
+        soa_ld<D>(elems, c, k - s, E, gk);
 #pragma unroll
         for (int r = 0; r < D; ++r) {
-          double acc = elems.g[k * D + r];
+          double acc = gk[r];
 #pragma unroll
           for (int j = 0; j < D; ++j) acc = fma(E[r][j], mu[j], acc);
           nm[r] = acc;

@@ -278,6 +278,45 @@ __device__ __forceinline__ bool combine_filtering(const Grp<D>& g, const FEl<D>&
   return !sing;
 }
 
+// Gaussian-carry ⊗_f: (0, b_i, C_i, 0, 0) ⊗ rj -> (0, b, C, 0, 0).  Every
+// prefix of a sequence whose first element absorbed the initial
+// distribution has this form (parallel.cpp:13-24, 92-98), so the down-sweep
+// of the IEKS aggregate scan only needs b and C: A, eta and J (and the
+// J-side triangularisation) are skipped.
+template <int D>
+__device__ __forceinline__ bool combine_gauss(const Grp<D>& g, double bi, const Rw<D>& ci, const FEl<D>& rj,
+                                              double& bo, Rw<D>& co) {
+  constexpr int K = 2 * D;
+  Rw<K> top, bot;
+  const Rw<D> x = mm_tn(g, ci, rj.j);  // C_i^T J_j
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    top[j] = x[j];
+    top[D + j] = (j == g.r) ? 1.0 : 0.0;
+    bot[j] = rj.j[j];
+    bot[D + j] = 0.0;
+  }
+  lq<D, D, 0, K>(g, top, bot);
+  const bool sing = singular_diag(g, pick(top, g.r), D);
+  Rw<D> xi11, xi21;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    xi11[j] = top[j];
+    xi21[j] = bot[j];
+  }
+  publish_factor<D, D>(g, xi11);
+  const Rw<D> w = solve_xlt<D, D>(g, ci);  // W = C_i Xi11^-T
+  Rw<D> gm = mm_nt(g, w, xi21);
+#pragma unroll
+  for (int j = 0; j < D; ++j) gm[j] = ((j == g.r) ? 1.0 : 0.0) - gm[j];
+  const Rw<D> ag = mm(g, rj.a, gm);
+  const double t1 = matvec_t(g, ci, rj.eta);
+  const double t2 = matvec(g, ci, t1);
+  bo = matvec(g, ag, bi + t2) + rj.b;
+  co = sqrt_sum(g, mm(g, rj.a, w), rj.c);
+  return !sing;
+}
+
 // ------------------------------------------------------ smoothing element ---
 // make_smoothing_element (parallel.cpp:112-135).
 template <int D>
