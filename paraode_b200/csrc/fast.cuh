@@ -45,7 +45,9 @@ struct FastConst {
 
 struct FastArgs {
   const double* grid;   // N+1 nodes
-  const double* eta;    // (N+1) x D linearisation points (original coordinates)
+  const double* eta;    // linearisation points (original coordinates): (N+1) x D row-major for the
+                        // group passes; chunk-interleaved (lane::eta_at) for the lane passes
+  const double* eta_term;  // lane layout: node N
   int64_t N;
   int L;
   int64_t nchunks;

@@ -146,11 +146,9 @@ struct Model {
     double off[d];
     bool finite;
   };
-  __device__ static Lin linearize(const DevProblem& prob, const double* eta, int ek0) {
+  __device__ static Lin linearize(const DevProblem& prob, const double (&y)[d], int ek0) {
     Lin l;
-    double y[d], f[d], jac[d * d];
-#pragma unroll
-    for (int j = 0; j < d; ++j) y[j] = eta[j * B];
+    double f[d], jac[d * d];
     eval_field<d>(prob, y, f, jac);
     bool fin = true;
 #pragma unroll
@@ -316,6 +314,28 @@ struct ElemSoA {
   int L;
 };
 
+// The trajectory eta in the same chunk-interleaved layout: component r of
+// node k = c L + t (k < N) at (t * D + r) * nc + c; node N in `term`.
+template <int D>
+__device__ __forceinline__ int64_t eta_index(int64_t k, int r, int L, int64_t nc) {
+  const int64_t c = k / L;
+  return ((k - c * L) * D + r) * nc + c;
+}
+
+template <int D>
+__device__ __forceinline__ double eta_at(const double* base, const double* term, int64_t k, int r, int64_t N,
+                                         int L, int64_t nc) {
+  return (k == N) ? term[r] : base[eta_index<D>(k, r, L, nc)];
+}
+
+// y = E_0 eta_k (the solution components of node k).
+template <int D, int d>
+__device__ __forceinline__ void gather_y(const FastArgs& a, int64_t k, double (&y)[d]) {
+  constexpr int B = D / d;
+#pragma unroll
+  for (int j = 0; j < d; ++j) y[j] = eta_at<D>(a.eta, a.eta_term, k, j * B, a.N, a.L, a.nchunks);
+}
+
 template <int D>
 __device__ __forceinline__ void soa_st(const ElemSoA& s, int64_t c, int64_t t, const double (&E)[D][D],
                                        const double (&g)[D]) {
@@ -392,7 +412,9 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(FastArgs a, Fa
     double cm[D][D];
     M::predict_cov(pc, C, cst.q, cm);
     // update at node k+1
-    const typename M::Lin lin = M::linearize(a.prob, a.eta + (k + 1) * D, a.ek0);
+    double ylin[d];
+    gather_y<D, d>(a, k + 1, ylin);
+    const typename M::Lin lin = M::linearize(a.prob, ylin, a.ek0);
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
     const typename M::Upd u = M::update(lin, tn, cm);
     bad_sing |= u.singular;
@@ -566,7 +588,9 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
     }
     soa_st<D>(elems, c, k - s, E, gk);
     // measurement update at node k+1
-    const typename M::Lin lin = M::linearize(a.prob, a.eta + (k + 1) * D, a.ek0);
+    double ylin[d];
+    gather_y<D, d>(a, k + 1, ylin);
+    const typename M::Lin lin = M::linearize(a.prob, ylin, a.ek0);
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
     const typename M::Upd u = M::update(lin, tn, cm);
     bad_sing |= u.singular;
@@ -647,15 +671,20 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_bfold(ElemSoA elems, int6
 // One thread per chunk: backward mean recursion m_n = g_n + E_n m_{n+1}
 // from the chunk's incoming smoothed mean; new trajectory (original
 // coordinates) and per-chunk objective / stopping partials.
+// eta_old / eta_new (and their node-N slots) are in the chunk-interleaved
+// layout of eta_at; the next step's (E, g, eta_old) are prefetched while the
+// current step computes.
 template <int D, int d, bool kInitial>
 __global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, FastConst<D> cst, ElemSoA elems,
                                                                 SEd suffix, const double* eta_old,
-                                                                double* eta_new, double* part) {
+                                                                const double* old_term, double* eta_new,
+                                                                double* new_term, double* part) {
   using M = Model<D, d>;
   constexpr int B = M::B;
   __shared__ double red[3][kLaneThreads];
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   const bool okc = c < a.nchunks;
+  const int64_t nc = a.nchunks;
   double obj = 0.0, dmax = 0.0, emax = 0.0;
   if (okc) {
     const int64_t s = c * a.L;
@@ -667,16 +696,17 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, Fast
 #pragma unroll
     for (int r = 0; r < D; ++r) {
       double eta_e;
+      const double old_e = eta_at<D>(eta_old, old_term, e, r, a.N, a.L, nc);
       if (kInitial) {
-        eta_e = eta_old[e * D + r];
+        eta_e = old_e;
         mu[r] = 0.0;
       } else {
         mu[r] = last ? elems.term[r] : suffix.g[(c + 1) * D + r];
         eta_e = te[r % B] * mu[r];
       }
       if (last) {
-        if (!kInitial) eta_new[a.N * D + r] = eta_e;
-        dmax = fmax(dmax, fabs(eta_e - eta_old[a.N * D + r]));
+        if (!kInitial) new_term[r] = eta_e;
+        dmax = fmax(dmax, fabs(eta_e - old_e));
         emax = fmax(emax, fabs(eta_e));
       }
       bar_next[r] = tei[r % B] * eta_e;
@@ -684,16 +714,35 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, Fast
     double tn[B];
 #pragma unroll
     for (int i = 0; i < B; ++i) tn[i] = tei[i];  // T_{k+1}^-1
+    // prefetch of step k = e - 1
+    double En[D][D], gn[D], on[D];
+    if (e - 1 >= s) {
+      if (!kInitial) soa_ld<D>(elems, c, e - 1 - s, En, gn);
+#pragma unroll
+      for (int r = 0; r < D; ++r) on[r] = eta_old[((e - 1 - s) * D + r) * nc + c];
+    }
     for (int64_t k = e - 1; k >= s; --k) {
+      double E[D][D], gk[D], oldk[D];
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        gk[r] = gn[r];
+        oldk[r] = on[r];
+#pragma unroll
+        for (int j = 0; j < D; ++j) E[r][j] = En[r][j];
+      }
+      if (k - 1 >= s) {
+        if (!kInitial) soa_ld<D>(elems, c, k - 1 - s, En, gn);
+#pragma unroll
+        for (int r = 0; r < D; ++r) on[r] = eta_old[((k - 1 - s) * D + r) * nc + c];
+      }
       double tk[B], tki[B];
       M::taus(a.grid, k, tk, tki);
       double etak[D];
       if (kInitial) {
 #pragma unroll
-        for (int r = 0; r < D; ++r) etak[r] = eta_old[k * D + r];
+        for (int r = 0; r < D; ++r) etak[r] = oldk[r];
       } else {
-        double E[D][D], gk[D], nm[D];
-        soa_ld<D>(elems, c, k - s, E, gk);
+        double nm[D];
 #pragma unroll
         for (int r = 0; r < D; ++r) {
           double acc = gk[r];
@@ -705,13 +754,13 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, Fast
         for (int r = 0; r < D; ++r) {
           mu[r] = nm[r];
           etak[r] = tk[r % B] * nm[r];
-          eta_new[k * D + r] = etak[r];
+          eta_new[((k - s) * D + r) * nc + c] = etak[r];
         }
       }
       double bar[D];
 #pragma unroll
       for (int r = 0; r < D; ++r) {
-        dmax = fmax(dmax, fabs(etak[r] - eta_old[k * D + r]));
+        dmax = fmax(dmax, fabs(etak[r] - oldk[r]));
         emax = fmax(emax, fabs(etak[r]));
         bar[r] = tki[r % B] * etak[r];
       }

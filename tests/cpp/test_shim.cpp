@@ -62,6 +62,8 @@ int main() {
     auto rep = pb::para_ieks<Mat, Vec>(p, pb::IwpPrior{2, 1, 1.0}, grid, pb::IeksConfig{}, gpu);
     CHECK(rep.converged);
     const double want = 0.01 / (0.01 + 0.99 * std::exp(-10.0));
+    std::printf("logistic: iterations %d, y(10) = %.12f (want %.12f), sigma_hat %.6g\n", rep.iterations,
+                rep.solution_means.back()[0], want, rep.sigma_hat);
     CHECK(std::fabs(rep.solution_means.back()[0] - want) <= 1e-4);
     CHECK(rep.sigma_hat > 0.0);
     CHECK(rep.objective_trace.size() == size_t(rep.iterations));
