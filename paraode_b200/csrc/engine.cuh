@@ -376,7 +376,8 @@ __global__ void __launch_bounds__(kThreads) k_scan_reduce_loc(FEd x, int64_t n, 
     const bool ok = okc && k < hi;
     const FEl<D> e = FOps<D>::load(x, k, g.r, ok);
     FEl<D> tmp;
-    const bool good = combine_filtering<D>(g, acc, e, tmp);
+    // IEKS aggregates carry lower-triangular C and J (tria outputs)
+    const bool good = combine_filtering<D, true>(g, acc, e, tmp);
     bad |= ok && !good;
     acc = FOps<D>::select(ok, tmp, acc);
     FOps<D>::store(loc, k, g.r, ok, acc);

@@ -218,11 +218,19 @@ __device__ __forceinline__ Rw<D> transpose(const Grp<D>& g, const Rw<D>& a) {
 // the rows hold L (lower triangular in pivot order); L L^T = M M^T.
 // Sum of squares of x[lo..K) with four independent accumulators (short
 // dependency chains; every lane evaluates it identically).
-template <int K>
-__device__ __forceinline__ double sumsq_from(const Rw<K>& x, int lo) {
+// Structural sparsity of the stacked trias [L | T] used here: when the right
+// block (columns >= S) is lower triangular in every row, then before pivot p
+// every row is zero in columns > S + p (each pivot row's reflector only
+// reaches S + p, by induction), so those columns are skipped.  S = K means
+// no structure.  (Pure zeros are skipped: the arithmetic is unchanged.)
+__device__ __forceinline__ constexpr bool live_col(int j, int p, int S) { return j < S || j <= S + p; }
+
+template <int K, int S = K>
+__device__ __forceinline__ double sumsq_from(const Rw<K>& x, int lo, int p) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
   for (int j = lo; j < K; ++j) {
+    if (!live_col(j, p, S)) continue;
     const int s = (j - lo) & 3;
     if (s == 0) a0 = fma(x[j], x[j], a0);
     if (s == 1) a1 = fma(x[j], x[j], a1);
@@ -232,11 +240,12 @@ __device__ __forceinline__ double sumsq_from(const Rw<K>& x, int lo) {
   return (a0 + a1) + (a2 + a3);
 }
 
-template <int K>
-__device__ __forceinline__ double dot_from(const Rw<K>& x, const Rw<K>& y, int lo, double init) {
+template <int K, int S = K>
+__device__ __forceinline__ double dot_from(const Rw<K>& x, const Rw<K>& y, int lo, double init, int p) {
   double a0 = init, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
   for (int j = lo; j < K; ++j) {
+    if (!live_col(j, p, S)) continue;
     const int s = (j - lo) & 3;
     if (s == 0) a0 = fma(x[j], y[j], a0);
     if (s == 1) a1 = fma(x[j], y[j], a1);
@@ -297,45 +306,47 @@ __device__ __forceinline__ void householder_coefs(double c0, double tail, double
   inv = live ? ic : 0.0;
 }
 
-template <int K>
+template <int K, int S = K>
 __device__ __forceinline__ Reflector<K> make_reflector(const Rw<K>& x, int p) {
   Reflector<K> h;
-  const double tail = sumsq_from(x, p + 1);
+  const double tail = sumsq_from<K, S>(x, p + 1, p);
   double inv;
   householder_coefs(x[p], tail, h.tau, h.beta, inv);
 #pragma unroll
-  for (int j = p + 1; j < K; ++j) h.ess[j] = x[j] * inv;
+  for (int j = p + 1; j < K; ++j) h.ess[j] = live_col(j, p, S) ? x[j] * inv : 0.0;
   return h;
 }
 
 // y <- y (I - tau v v^T), v = [1, ess] on columns p..K-1.
-template <int K>
+template <int K, int S = K>
 __device__ __forceinline__ void apply_reflector(const Reflector<K>& h, int p, Rw<K>& y) {
-  const double w = dot_from(y, h.ess, p + 1, y[p]);
+  const double w = dot_from<K, S>(y, h.ess, p + 1, y[p], p);
   const double tw = h.tau * w;
   y[p] -= tw;
 #pragma unroll
-  for (int j = p + 1; j < K; ++j) y[j] = fma(-tw, h.ess[j], y[j]);
+  for (int j = p + 1; j < K; ++j)
+    if (live_col(j, p, S)) y[j] = fma(-tw, h.ess[j], y[j]);
 }
 
 // Row p of a register row set, fetched from its owner lane.
-template <int D, int K>
+template <int D, int K, int S = K>
 __device__ __forceinline__ Rw<K> shfl_row(const Grp<D>& g, const Rw<K>& row, int owner, int from) {
   const int src = (threadIdx.x & 31) - g.r + owner;
   Rw<K> x;
 #pragma unroll
-  for (int j = 0; j < K; ++j) x[j] = (j >= from) ? __shfl_sync(0xffffffffu, row[j], src) : 0.0;
+  for (int j = 0; j < K; ++j)
+    x[j] = (j >= from && live_col(j, from, S)) ? __shfl_sync(0xffffffffu, row[j], src) : 0.0;
   return x;
 }
 
-template <int D, int NT, int NB, int K>
+template <int D, int NT, int NB, int K, int S = K>
 __device__ __forceinline__ void lq(const Grp<D>& g, Rw<K>& top, Rw<K>& bot) {
   constexpr int kPivots = (NT + NB < K) ? (NT + NB) : K;
 #pragma unroll
   for (int p = 0; p < kPivots; ++p) {
     const bool in_top = p < NT;
     const int owner = in_top ? p : p - NT;
-    const Reflector<K> h = make_reflector(shfl_row(g, in_top ? top : bot, owner, p), p);
+    const Reflector<K> h = make_reflector<K, S>(shfl_row<D, K, S>(g, in_top ? top : bot, owner, p), p);
     const double tau = h.tau;
     const double beta = h.beta;
     const Rw<K>& ess = h.ess;
@@ -349,15 +360,15 @@ __device__ __forceinline__ void lq(const Grp<D>& g, Rw<K>& top, Rw<K>& bot) {
     // becomes [.., beta, 0, ..] (branch-free select, no divergence).
     const bool own = g.r == owner;
     if (in_top) {
-      apply_reflector(h, p, top);
-      apply_reflector(h, p, bot);
+      apply_reflector<K, S>(h, p, top);
+      apply_reflector<K, S>(h, p, bot);
       if (own) {
         top[p] = beta;
 #pragma unroll
         for (int j = p + 1; j < K; ++j) top[j] = 0.0;
       }
     } else {
-      apply_reflector(h, p, bot);
+      apply_reflector<K, S>(h, p, bot);
       if (own) {
         bot[p] = beta;
 #pragma unroll
@@ -369,15 +380,15 @@ __device__ __forceinline__ void lq(const Grp<D>& g, Rw<K>& top, Rw<K>& bot) {
 
 // Two independent LQs of D x K row sets run in one pivot sweep (their
 // reflectors are independent, so the two dependency chains overlap).
-template <int D, int K>
+template <int D, int K, int S = K>
 __device__ __forceinline__ void lq_pair(const Grp<D>& g, Rw<K>& a, Rw<K>& b) {
   constexpr int kPivots = (D < K) ? D : K;
 #pragma unroll
   for (int p = 0; p < kPivots; ++p) {
-    const Reflector<K> ha = make_reflector(shfl_row(g, a, p, p), p);
-    const Reflector<K> hb = make_reflector(shfl_row(g, b, p, p), p);
-    apply_reflector(ha, p, a);
-    apply_reflector(hb, p, b);
+    const Reflector<K> ha = make_reflector<K, S>(shfl_row<D, K, S>(g, a, p, p), p);
+    const Reflector<K> hb = make_reflector<K, S>(shfl_row<D, K, S>(g, b, p, p), p);
+    apply_reflector<K, S>(ha, p, a);
+    apply_reflector<K, S>(hb, p, b);
     if (g.r == p) {
       a[p] = ha.beta;
       b[p] = hb.beta;
@@ -391,17 +402,17 @@ __device__ __forceinline__ void lq_pair(const Grp<D>& g, Rw<K>& a, Rw<K>& b) {
 }
 
 // Single row set: tria of a D x K matrix (K >= D) -> rows of L (first D cols).
-template <int D, int K>
+template <int D, int K, int S = K>
 __device__ __forceinline__ Rw<D> tria(const Grp<D>& g, Rw<K> m) {
   Rw<K> none = zeros<K>();
-  lq<D, 0, D, K>(g, none, m);
+  lq<D, 0, D, K, S>(g, none, m);
   Rw<D> o;
 #pragma unroll
   for (int j = 0; j < D; ++j) o[j] = m[j];
   return o;
 }
 
-// sqrt_sum(A, B) = tria([A B]) for D x D factors.
+// sqrt_sum(A, B) = tria([A B]) for D x D factors (general B).
 template <int D>
 __device__ __forceinline__ Rw<D> sqrt_sum(const Grp<D>& g, const Rw<D>& a, const Rw<D>& b) {
   Rw<2 * D> m;
@@ -411,6 +422,18 @@ __device__ __forceinline__ Rw<D> sqrt_sum(const Grp<D>& g, const Rw<D>& a, const
     m[D + j] = b[j];
   }
   return tria<D, 2 * D>(g, m);
+}
+
+// sqrt_sum for a lower-triangular B (skips its structural zeros).
+template <int D>
+__device__ __forceinline__ Rw<D> sqrt_sum_lt(const Grp<D>& g, const Rw<D>& a, const Rw<D>& b) {
+  Rw<2 * D> m;
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    m[j] = a[j];
+    m[D + j] = b[j];
+  }
+  return tria<D, 2 * D, D>(g, m);
 }
 
 // ----------------------------------------------------- triangular solves ---

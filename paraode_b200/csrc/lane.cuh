@@ -30,13 +30,16 @@ constexpr int kLaneThreads = 128;
 // pivots: row p is reflected against columns p..K-1 and every later row is
 // updated (Eigen convention: beta = -sign(c0) ||x||, tau = (beta - c0) / beta,
 // essential = tail / (c0 - beta); identity when ||tail||^2 <= DBL_MIN).
-template <int R, int K, int P>
+// S < K: the right block (columns >= S) is lower triangular, so columns
+// > S + p are structurally zero at pivot p and skipped (group.cuh live_col).
+template <int R, int K, int P, int S = K>
 __device__ __forceinline__ void lq(double (&m)[R][K]) {
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     double t0 = 0.0, t1 = 0.0;
 #pragma unroll
     for (int j = p + 1; j < K; ++j) {
+      if (!live_col(j, p, S)) continue;
       if ((j - p) & 1)
         t0 = fma(m[p][j], m[p][j], t0);
       else
@@ -47,12 +50,13 @@ __device__ __forceinline__ void lq(double (&m)[R][K]) {
     householder_coefs(m[p][p], tail, tau, beta, inv);  // branch-free (group.cuh)
     double ess[K];
 #pragma unroll
-    for (int j = p + 1; j < K; ++j) ess[j] = m[p][j] * inv;
+    for (int j = p + 1; j < K; ++j) ess[j] = live_col(j, p, S) ? m[p][j] * inv : 0.0;
 #pragma unroll
     for (int r = p + 1; r < R; ++r) {
       double w0 = m[r][p], w1 = 0.0;
 #pragma unroll
       for (int j = p + 1; j < K; ++j) {
+        if (!live_col(j, p, S)) continue;
         if ((j - p) & 1)
           w1 = fma(m[r][j], ess[j], w1);
         else
@@ -61,7 +65,8 @@ __device__ __forceinline__ void lq(double (&m)[R][K]) {
       const double tw = tau * (w0 + w1);
       m[r][p] -= tw;
 #pragma unroll
-      for (int j = p + 1; j < K; ++j) m[r][j] = fma(-tw, ess[j], m[r][j]);
+      for (int j = p + 1; j < K; ++j)
+        if (live_col(j, p, S)) m[r][j] = fma(-tw, ess[j], m[r][j]);
     }
     // when tau == 0 (tail below DBL_MIN) this is the identity with beta = c0;
     // the tail is dropped, as Eigen's triangular view of R drops it
@@ -280,7 +285,7 @@ struct Model {
     for (int r = 0; r < D; ++r)
 #pragma unroll
       for (int j = 0; j < D; ++j) m[r][j] = left[r][j];
-    lq<D, 2 * D, D>(m);
+    lq<D, 2 * D, D, D>(m);  // right block Q^1/2: lower triangular
 #pragma unroll
     for (int r = 0; r < D; ++r)
 #pragma unroll

@@ -217,7 +217,7 @@ __device__ __forceinline__ bool first_filtering_element(const Grp<D>& g, const G
 }
 
 // ⊗_f (parallel.cpp:67-100).
-template <int D>
+template <int D, bool kTri = false>
 __device__ __forceinline__ bool combine_filtering(const Grp<D>& g, const FEl<D>& li, const FEl<D>& rj,
                                                   FEl<D>& out) {
   constexpr int K = 2 * D;
@@ -233,7 +233,7 @@ __device__ __forceinline__ bool combine_filtering(const Grp<D>& g, const FEl<D>&
   // Only the first D pivots are needed: they give Xi11 and Xi21, and the
   // remaining bottom block R satisfies R R^T = Xi22 Xi22^T (any factor of
   // Xi22 serves, since it only enters J through another tria).
-  lq<D, D, 0, K>(g, top, bot);
+  lq<D, D, 0, K, D>(g, top, bot);  // right block [I; 0]: lower triangular
   const bool sing = singular_diag(g, pick(top, g.r), D);
   Rw<D> xi11, xi21, xi22;
 #pragma unroll
@@ -269,7 +269,10 @@ __device__ __forceinline__ bool combine_filtering(const Grp<D>& g, const FEl<D>&
     sc_j[j] = ax[j];
     sc_j[D + j] = li.j[j];
   }
-  lq_pair<D, 2 * D>(g, sc_c, sc_j);
+  // right blocks C_j, J_i: lower triangular only when the elements come from
+  // this library's own trias (kTri); reference-format elements carry a
+  // general J (parallel.hpp:20-26)
+  lq_pair<D, 2 * D, kTri ? D : 2 * D>(g, sc_c, sc_j);
 #pragma unroll
   for (int j = 0; j < D; ++j) {
     out.c[j] = sc_c[j];
@@ -296,7 +299,7 @@ __device__ __forceinline__ bool combine_gauss(const Grp<D>& g, double bi, const 
     bot[j] = rj.j[j];
     bot[D + j] = 0.0;
   }
-  lq<D, D, 0, K>(g, top, bot);
+  lq<D, D, 0, K, D>(g, top, bot);  // right block [I; 0]: lower triangular
   const bool sing = singular_diag(g, pick(top, g.r), D);
   Rw<D> xi11, xi21;
 #pragma unroll
@@ -313,7 +316,7 @@ __device__ __forceinline__ bool combine_gauss(const Grp<D>& g, double bi, const 
   const double t1 = matvec_t(g, ci, rj.eta);
   const double t2 = matvec(g, ci, t1);
   bo = matvec(g, ag, bi + t2) + rj.b;
-  co = sqrt_sum(g, mm(g, rj.a, w), rj.c);
+  co = sqrt_sum_lt(g, mm(g, rj.a, w), rj.c);  // C_j: a tria output (IEKS aggregates)
   return !sing;
 }
 
