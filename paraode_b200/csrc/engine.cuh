@@ -523,7 +523,10 @@ struct Engine {
     const size_t sm = smem_bytes<D>();
     FEd loc = alloc<FOps<D>>(ctx, "gscan_loc_" + std::to_string(level), n);
     if (n <= L) {
-      k_scan_reduce_loc<D><<<1, kThreads, sm, ctx->stream>>>(in, n, static_cast<int>(n), loc, loc, err);
+      // the single chunk's aggregate goes to a scratch slot: loc[0] must stay
+      // the first element's own prefix
+      FEd top = alloc<FOps<D>>(ctx, "gscan_top", 1);
+      k_scan_reduce_loc<D><<<1, kThreads, sm, ctx->stream>>>(in, n, static_cast<int>(n), loc, top, err);
       note_launch(ctx, "scan_g_reduce");
       t.combines += n - 1;
       t.depth += n - 1;

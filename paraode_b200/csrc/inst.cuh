@@ -36,7 +36,10 @@ void rt(pode_context* c, const DevChain& ch, double* fm, double* fc, double* sm,
   *t = E::rts(c, ch, fm, fc, sm, sc);
 }
 template <int DD, int d>
-constexpr bool kFastOk = (d <= 3) && (DD % d == 0) && (DD / d >= 2) && (DD / d <= 5);
+// Lane-serial passes keep D x D matrices in registers: beyond D = 9 they
+// spill heavily (and take tens of minutes to compile), so larger states use
+// the group engine.
+constexpr bool kFastOk = (d <= 3) && (DD % d == 0) && (DD / d >= 2) && (DD / d <= 5) && (DD <= 9);
 
 // The fused engine (fast.cuh) serves ODE information operators with d <= 3;
 // everything else (and PODE_IEKS_ENGINE=elements) runs the element/scan
