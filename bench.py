@@ -90,6 +90,60 @@ def kernel_model(D, d):
     }
 
 
+def combine_flops(D):
+    """⊗_f dense-op flops (30 1/3 D^3 + 20 D^2; 7.27 k at D=6)
+    and the Gaussian-carry combine (A = eta = J = 0 on the left: 5.3 k at
+    D=6, same ratio)."""
+    full = 30.0 + 1.0 / 3.0
+    f = full * D ** 3 + 20 * D * D
+    return f, f * 5.3 / 7.27
+
+
+def sklansky_readers(cnt):
+    """Combines a Sklansky scan of cnt elements needs (readers per step)."""
+    tot, h = 0, 1
+    while h < cnt:
+        tot += sum(1 for p in range(cnt) if p & h)
+        h <<= 1
+    return tot
+
+
+def scan_model(N, D, sm=148, fanin=4):
+    """Algorithmic (flops, bytes) per IEKS iteration of the aggregate-scan
+    kernels, replaying fast_driver.cuh's tree: chunk length L (one chunk per
+    lane thread), level 0 sequential fan-in, upper levels block-Sklansky of
+    G = 8 * (32 // D) elements (engine.cuh)."""
+    L = max(8, min(-(-N // (sm * 256)), 4096))
+    nc = -(-N // L)
+    G = 8 * (32 // D)
+    f_full, f_gauss = combine_flops(D)
+    f_aff = 2 * D ** 3 + 2 * D * D  # mean-only ⊗_s (E, g)
+    el_f, el_m = 8 * (3 * D * D + 2 * D), 8 * (D * D + D)
+    out = {}
+
+    def add(k, fl, by):
+        a = out.setdefault(k, [0.0, 0.0])
+        a[0] += fl
+        a[1] += by
+    # level 0: fan-in reduce with local prefixes, then the one-deep down-sweep
+    add("scan_g_reduce", (nc - -(-nc // fanin)) * f_full, 2 * nc * el_f)
+    add("scan_m_reduce", (nc - -(-nc // fanin)) * f_aff, 2 * nc * el_m)
+    n = -(-nc // fanin)
+    downs = [(nc, fanin)] if n > 1 else []
+    while n > 1:
+        nb = -(-n // G)
+        work = sum(sklansky_readers(min(G, n - b * G)) for b in range(nb))
+        add("bscan_g", work * f_full, 2 * n * el_f)
+        add("bscan_m", work * f_aff, 2 * n * el_m)
+        if nb > 1:
+            downs.append((n, G))
+        n = nb
+    for m, c in downs:
+        add("scan_g_down", (m - min(m, c)) * f_gauss, m * (el_f + 8 * (D + D * D)))
+        add("scan_m_down", (m - min(m, c)) * (2 * D * D), m * (el_m + 8 * D))
+    return out
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -263,34 +317,57 @@ def run_ours(args):
     if rank != 0:
         return
 
-    # roofline of the dominant kernel (largest share of the timed region)
+    # roofline of the dominant kernel (largest share of the timed region):
+    # algorithmic flops / HBM bytes of everything that kernel name did in the
+    # timed region (lane passes: per-step counts x N x iterations; scan trees:
+    # per-iteration tree counts x iterations) / its summed event time.
     hbm, hbm_src, fp64, fp64_src = peaks()
-    model = kernel_model(D, d)
+    per_step = kernel_model(D, d)
+    per_iter = scan_model(n, D)
     total_ms = sum(v[1] for v in prof.values())
-    dom = max(prof.items(), key=lambda kv: kv[1][1])
-    name, (cnt, kms) = dom
-    avg_s = kms / cnt * 1e-3
-    roof = {"kernel": name, "share_of_step": kms / total_ms if total_ms else None}
-    if name in model:
-        flops, bytes_ = model[name]
-        t_fp64 = flops * n / (fp64 * 1e12)
-        t_hbm = bytes_ * n / (hbm * 1e9)
+    solves = args.steps
+
+    def work(name):
+        if name in per_step:
+            fl, by = per_step[name]
+            return fl * n * iters * solves, by * n * iters * solves
+        if name in per_iter:
+            fl, by = per_iter[name]
+            return fl * iters * solves, by * iters * solves
+        return None
+
+    def roofline(name):
+        cnt, kms = prof[name]
+        r = {"kernel": name, "share_of_step": kms / total_ms if total_ms else None, "launches": cnt,
+             "avg_launch_ms": kms / cnt}
+        w = work(name)
+        if w is None:
+            return r
+        fl, by = w
+        t = kms * 1e-3
         traffic = None
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
             traffic = tr.get(f"{name}@2^{args.log2n}")
         except Exception:
             pass
-        if t_fp64 >= t_hbm:
-            achieved = flops * n / avg_s / 1e12
-            roof.update({"bound": "fp64", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
-                         "frac": achieved / fp64, "peak_source": fp64_src})
+        if fl / (fp64 * 1e12) >= by / (hbm * 1e9):
+            a = fl / t / 1e12
+            r.update({"bound": "fp64", "achieved": a, "peak": fp64, "unit": "TFLOP/s", "frac": a / fp64,
+                      "peak_source": fp64_src})
         else:
-            achieved = bytes_ * n / avg_s / 1e9
-            roof.update({"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "peak_source": hbm_src})
-        roof.update({"traffic": traffic, "algorithmic_flops_per_launch": flops * n,
-                     "algorithmic_bytes_per_launch": bytes_ * n, "avg_launch_ms": avg_s * 1e3})
+            a = by / t / 1e9
+            r.update({"bound": "hbm", "achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm,
+                      "peak_source": hbm_src})
+        r.update({"traffic": traffic, "algorithmic_flops_per_launch": fl / cnt,
+                  "algorithmic_bytes_per_launch": by / cnt})
+        return r
+
+    dom = max(prof.items(), key=lambda kv: kv[1][1])[0]
+    roof = roofline(dom)
+    ranked = sorted(prof.items(), key=lambda kv: -kv[1][1])[:8]
+    roof_all = {k: {kk: vv for kk, vv in roofline(k).items() if kk in ("share_of_step", "bound", "achieved", "unit", "frac")}
+                for k, _ in ranked}
     kernels = {k: {"launches": c, "ms_per_step": t / args.steps} for k, (c, t) in sorted(prof.items())}
     line = {"metric": METRIC, "value": value, "unit": "time-steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -301,7 +378,7 @@ def run_ours(args):
                        "parallelism": f"replicas x{world}", "l2": "working set > L2 (126 MB) per solve"},
             "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof,
             "e2e": {"value": e2e, "unit": "time-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-            "kernels": kernels, "ms_per_step_profiled": ms_prof}
+            "kernels": kernels, "roofline_top_kernels": roof_all, "ms_per_step_profiled": ms_prof}
     if not args.no_cpu_baseline:
         t, it = cpu_solve(args.problem, nu, CPU_SAMPLE_N, 0)
         line["cpu_baseline"] = {"value": CPU_SAMPLE_N / t, "unit": "time-steps/s", "cores": 1, "kind": "port",

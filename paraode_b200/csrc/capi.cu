@@ -2,6 +2,7 @@
 // staging, dispatch to the per-D engines and the mapping of device error
 // words onto the reference's exception types.
 #include <cuda_runtime.h>
+#include <omp.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -129,10 +130,53 @@ T* stage_in(pode_context* ctx, const std::string& tag, const T* src, size_t coun
   return d;
 }
 
+// Large device->host copies into caller (pageable) memory: DMA into a pinned
+// two-slot staging ring while host threads copy the previous slot out (the
+// caller's first-touch page faults are taken in parallel, not by the DMA
+// engine's pageable path).
+constexpr size_t kStageBytes = size_t(32) << 20;
+
+void copy_out_staged(pode_context* ctx, char* dst, const char* dev, size_t bytes) {
+  cudaStream_t st = ctx->stream;
+  for (int k = 0; k < 2; ++k) {
+    if (ctx->h_stage[k] == nullptr) {
+      cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_stage[k]), kStageBytes, cudaHostAllocDefault),
+                 "staging");
+      cuda_check(cudaEventCreateWithFlags(&ctx->stage_ev[k], cudaEventDisableTiming), "staging event");
+    }
+  }
+  const size_t n = (bytes + kStageBytes - 1) / kStageBytes;
+  auto issue = [&](size_t i) {
+    const size_t off = i * kStageBytes, len = std::min(kStageBytes, bytes - off);
+    cuda_check(cudaMemcpyAsync(ctx->h_stage[i & 1], dev + off, len, cudaMemcpyDeviceToHost, st), "copy out");
+    cuda_check(cudaEventRecord(ctx->stage_ev[i & 1], st), "copy out event");
+  };
+  issue(0);
+  if (n > 1) issue(1);
+  const int threads = std::max(1, std::min(8, omp_get_max_threads()));
+  for (size_t i = 0; i < n; ++i) {
+    cuda_check(cudaEventSynchronize(ctx->stage_ev[i & 1]), "copy out wait");
+    const size_t off = i * kStageBytes, len = std::min(kStageBytes, bytes - off);
+    const char* src = ctx->h_stage[i & 1];
+    const size_t per = (len + threads - 1) / threads;
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int t = 0; t < threads; ++t) {
+      const size_t lo = size_t(t) * per;
+      if (lo < len) std::memcpy(dst + off + lo, src + lo, std::min(per, len - lo));
+    }
+    if (i + 2 < n) issue(i + 2);
+  }
+}
+
 template <typename T>
 void stage_out(pode_context* ctx, T* dst, const T* dev, size_t count, bool device) {
   if (dst == nullptr || device) return;
-  cuda_check(cudaMemcpyAsync(dst, dev, sizeof(T) * count, cudaMemcpyDeviceToHost, ctx->stream), "copy out");
+  const size_t bytes = sizeof(T) * count;
+  if (bytes >= (size_t(4) << 20)) {
+    copy_out_staged(ctx, reinterpret_cast<char*>(dst), reinterpret_cast<const char*>(dev), bytes);
+    return;
+  }
+  cuda_check(cudaMemcpyAsync(dst, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream), "copy out");
 }
 
 void check_dims(int D, int64_t count) {
@@ -274,7 +318,13 @@ void pode_context_destroy(pode_context* ctx) {
   if (ctx == nullptr) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto& kv : ctx->ws.bufs)
+    if (kv.second.ptr) cudaFree(kv.second.ptr);
   ctx->ws.bufs.clear();
+  for (int k = 0; k < 2; ++k) {
+    if (ctx->h_stage[k]) cudaFreeHost(ctx->h_stage[k]);
+    if (ctx->stage_ev[k]) cudaEventDestroy(ctx->stage_ev[k]);
+  }
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);

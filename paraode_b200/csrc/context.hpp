@@ -80,6 +80,9 @@ struct pode_context {
   unsigned long long* h_err = nullptr;  // pinned mirror
   double* h_scalars = nullptr;          // pinned scalars (reductions)
   int64_t launches = 0;
+  // pinned staging ring for large device->host result copies (capi.cu)
+  char* h_stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   bool prof_on = false;
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> prof_pool;

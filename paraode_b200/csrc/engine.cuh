@@ -11,6 +11,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "context.hpp"
@@ -121,6 +122,10 @@ struct FOps {
   __device__ static bool combine(const Grp<D>& g, const El& l, const El& rr, El& out) {
     return combine_filtering<D>(g, l, rr, out);
   }
+  static constexpr int kDoubles = 3 * D * D + 2 * D;  // one element
+  __device__ static Arr smem_arr(double* buf, int n) {
+    return Arr{buf, buf + 3 * n * D * D, buf + n * D * D, buf + 3 * n * D * D + n * D, buf + 2 * n * D * D};
+  }
   __device__ static El select(bool take_a, const El& a, const El& b) {
     El o;
 #pragma unroll
@@ -194,6 +199,8 @@ struct MOps {
     out.g = matvec(g, l.e, rr.g) + l.g;
     return true;
   }
+  static constexpr int kDoubles = D * D + D;
+  __device__ static Arr smem_arr(double* buf, int n) { return Arr{buf, buf + n * D * D, nullptr}; }
   __device__ static El select(bool take_a, const El& a, const El& b) {
     El o;
 #pragma unroll
@@ -450,6 +457,75 @@ __global__ void __launch_bounds__(kThreads) k_mscan_down(SEd loc, int64_t n, int
   st_ent<D>(out.g, k, g.r, ok, last ? e.g : go);
 }
 
+// IEKS chunk aggregates: C and J are tria outputs (lower triangular).
+template <int D>
+struct FTOps : FOps<D> {
+  __device__ static bool combine(const Grp<D>& g, const FEl<D>& l, const FEl<D>& rr, FEl<D>& out) {
+    return combine_filtering<D, true>(g, l, rr, out);
+  }
+};
+
+// ---------------------------------------- block (Sklansky) local scans ---
+// The upper levels of the aggregate scans are latency-bound chains of
+// combines.  Here one CTA of kBWarps warps scans G = kBWarps * (32 / D)
+// consecutive elements with the Sklansky tree: log2(G) combine steps (every
+// group of a warp steps together, so the shuffles inside the combine stay
+// warp-uniform), elements exchanged through shared memory.  Produces the
+// block-local inclusive prefixes (suffixes when kRev) in loc and the block
+// aggregate in agg[blockIdx.x] — the same contract as k_scan_reduce_loc with
+// chunk length G, so the one-combine-deep down-sweeps are unchanged.
+constexpr int kBWarps = 8;
+
+template <int D>
+constexpr int bscan_groups() {
+  return kBWarps * Grp<D>::kPerWarp;
+}
+template <int D, class Op>
+constexpr size_t bscan_smem() {
+  return sizeof(double) *
+         (size_t(kBWarps) * Grp<D>::kSlots * Scratch<D>::kDoubles + size_t(bscan_groups<D>()) * Op::kDoubles);
+}
+
+template <int D, class Op, bool kRev>
+__global__ void __launch_bounds__(kBWarps * 32) k_bscan_loc(typename Op::Arr x, int64_t n, typename Op::Arr loc,
+                                                            typename Op::Arr agg, DevError* err) {
+  extern __shared__ double smem[];
+  constexpr int G = bscan_groups<D>();
+  const Grp<D> g = make_group<D>(smem);
+  const typename Op::Arr sb = Op::smem_arr(smem + kBWarps * Grp<D>::kSlots * Scratch<D>::kDoubles, G);
+  const int p = (threadIdx.x >> 5) * Grp<D>::kPerWarp + g.gw;  // position in the block
+  const bool real = g.real();
+  const int64_t lo = int64_t(blockIdx.x) * G;
+  const int64_t hi = min(n, lo + G);
+  const int cnt = int(hi - lo);
+  const bool ok = real && p < cnt;
+  const int64_t k = kRev ? hi - 1 - p : lo + p;
+  auto acc = Op::load(x, k, g.r, ok);
+  bool bad = false;
+#pragma unroll 1
+  for (int h = 1; h < cnt; h <<= 1) {  // cnt is block-uniform
+    // slot j is written once: at the step h = 2^(trailing ones of j)
+    if (real && (p & (2 * h - 1)) == h - 1) Op::store(sb, p, g.r, true, acc);
+    __syncthreads();
+    const bool rd = real && (p & h);
+    const int j = (p & ~(2 * h - 1)) + h - 1;
+    const auto left = Op::load(sb, rd ? j : 0, g.r, rd);
+    typename Op::El tmp;
+    const bool good = kRev ? Op::combine(g, acc, left, tmp) : Op::combine(g, left, acc, tmp);
+    bad |= rd && ok && !good;
+    acc = Op::select(rd, tmp, acc);
+  }
+  Op::store(loc, k, g.r, ok, acc);
+  if (ok && p == cnt - 1) Op::store(agg, blockIdx.x, g.r, true, acc);
+  if (ok && g.r == 0 && bad) raise_error(err, k, kErrSingular);
+}
+
+// Upper scan levels use the block kernel unless PODE_BSCAN=0.
+inline bool use_bscan() {
+  const char* env = std::getenv("PODE_BSCAN");
+  return env == nullptr || std::atoi(env) != 0;
+}
+
 // ------------------------------------------------------------- engine ---
 template <int D>
 struct Engine {
@@ -520,8 +596,35 @@ struct Engine {
   // down.
   static void scan_gauss_rec(pode_context* ctx, FEd in, FEd out, int64_t n, int level, int L, ScanTally& t) {
     DevError* err = reinterpret_cast<DevError*>(ctx->d_err);
-    const size_t sm = smem_bytes<D>();
+    size_t sm = smem_bytes<D>();
     FEd loc = alloc<FOps<D>>(ctx, "gscan_loc_" + std::to_string(level), n);
+    if (level >= 1 && use_bscan()) {  // block Sklansky levels
+      constexpr int G = bscan_groups<D>();
+      sm = bscan_smem<D, FOps<D>>();
+      static bool attr = false;
+      if (!attr) {
+        attr = true;
+        cuda_check(cudaFuncSetAttribute(k_bscan_loc<D, FTOps<D>, false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)),
+                   "bscan smem");
+      }
+      const int64_t nb = (n + G - 1) / G;
+      FEd agg = alloc<FOps<D>>(ctx, "gscan_agg_" + std::to_string(level), nb);
+      k_bscan_loc<D, FTOps<D>, false><<<unsigned(nb), kBWarps * 32, sm, ctx->stream>>>(in, n, nb == 1 ? out : loc,
+                                                                                     agg, err);
+      note_launch(ctx, "bscan_g");
+      int depth = 0;
+      while ((1 << depth) < std::min<int64_t>(n, G)) ++depth;
+      t.depth += depth;
+      t.combines += n * depth;
+      if (nb == 1) return;
+      scan_gauss_rec(ctx, agg, agg, nb, level + 1, L, t);
+      k_scan_down_gauss<D><<<blocks_for<D>(n), kThreads, smem_bytes<D>(), ctx->stream>>>(loc, n, G, agg, out, err);
+      note_launch(ctx, "scan_g_down");
+      t.combines += n - std::min<int64_t>(n, G);
+      t.depth += 1;
+      return;
+    }
     if (n <= L) {
       // the single chunk's aggregate goes to a scratch slot: loc[0] must stay
       // the first element's own prefix
@@ -566,8 +669,35 @@ struct Engine {
   // Reverse inclusive scan of mean-only elements ending in the terminal
   // element (E = 0): only the suffix means (out.g) are produced.
   static void mscan_rec(pode_context* ctx, SEd in, SEd out, int64_t n, int level, int L, ScanTally& t) {
-    const size_t sm = smem_bytes<D>();
+    size_t sm = smem_bytes<D>();
     SEd loc = alloc<SOps<D>>(ctx, "mscan_loc_" + std::to_string(level), n);
+    if (level >= 1 && use_bscan()) {  // block Sklansky levels
+      constexpr int G = bscan_groups<D>();
+      sm = bscan_smem<D, MOps<D>>();
+      static bool attr = false;
+      if (!attr) {
+        attr = true;
+        cuda_check(cudaFuncSetAttribute(k_bscan_loc<D, MOps<D>, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(sm)),
+                   "bscan smem");
+      }
+      const int64_t nb = (n + G - 1) / G;
+      SEd agg = alloc<SOps<D>>(ctx, "mscan_agg_" + std::to_string(level), nb);
+      k_bscan_loc<D, MOps<D>, true><<<unsigned(nb), kBWarps * 32, sm, ctx->stream>>>(in, n, nb == 1 ? out : loc,
+                                                                                    agg, nullptr);
+      note_launch(ctx, "bscan_m");
+      int depth = 0;
+      while ((1 << depth) < std::min<int64_t>(n, G)) ++depth;
+      t.depth += depth;
+      t.combines += n * depth;
+      if (nb == 1) return;
+      mscan_rec(ctx, agg, agg, nb, level + 1, L, t);
+      k_mscan_down<D><<<blocks_for<D>(n), kThreads, smem_bytes<D>(), ctx->stream>>>(loc, n, G, nb, agg, out);
+      note_launch(ctx, "scan_m_down");
+      t.combines += n - std::min<int64_t>(n, G);
+      t.depth += 1;
+      return;
+    }
     if (n <= L) {
       k_mscan_reduce_loc<D><<<1, kThreads, sm, ctx->stream>>>(in, n, static_cast<int>(n), loc, loc);
       note_launch(ctx, "scan_m_reduce");

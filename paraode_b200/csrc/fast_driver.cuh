@@ -12,7 +12,6 @@
 #include "fast.cuh"
 #include "ieks.cuh"
 #include "lane.cuh"
-#include "lane_scan.cuh"
 
 namespace pode {
 
@@ -39,14 +38,93 @@ __global__ void k_eta_rows(const double* base, const double* term, int64_t N, in
 
 }  // namespace lane
 
+// Device-side loop state of the graph-captured IEKS iteration.
+struct LoopState {
+  int it;         // completed iterations
+  int converged;
+  int max_it;
+  int pad;
+  double v_prev;  // objective of the previous iterate
+  double traj_rtol, obj_atol, obj_rtol;
+};
+
+// Per-iteration finish in graph-loop mode: the fixed-order reduction of the
+// pass-E partials (as k_finish3), the objective trace, the reference's
+// stopping rule (ieks.cpp:157-187) and the while-node condition; a device
+// error (singular factor / non-finite field) also ends the loop.
+static __global__ void k_finish_iter(const double* part, int64_t nparts, LoopState* ls, double* trace,
+                                     const unsigned long long* err, cudaGraphConditionalHandle h) {
+  double r[3];
+  finish3_block(part, nparts, r);
+  if (threadIdx.x != 0) return;
+  const double v = 0.5 * r[0];
+  trace[ls->it] = v;
+  const bool conv =
+      (r[1] <= ls->traj_rtol * r[2]) || (fabs(v - ls->v_prev) <= ls->obj_atol + ls->obj_rtol * fabs(v));
+  ls->v_prev = v;
+  ls->it += 1;
+  ls->converged = conv ? 1 : 0;
+  const bool failed = *err != ~0ull;
+  cudaGraphSetConditional(h, (!conv && !failed && ls->it < ls->max_it) ? 1u : 0u);
+}
+
 template <int D, int d>
 struct FastEngine {
-  // Chunk-aggregate scans: the group engine by default (its ⊗_f has the
-  // shorter critical path); PODE_SCAN_MODE=lane selects the lane-serial one.
-  static bool lane_scans() {
-    const char* env = std::getenv("PODE_SCAN_MODE");
-    return env != nullptr && std::string(env) == "lane";
+  // Iterations 2.. run as one CUDA graph with a device-side while node (no
+  // host round trip per iteration) unless profiling or PODE_GRAPH=0.
+  static bool use_graph(pode_context* ctx, const pode_ieks_config& cfg) {
+    const char* env = std::getenv("PODE_GRAPH");
+    return !ctx->prof_on && cfg.max_iterations > 1 && !(env != nullptr && std::atoi(env) == 0);
   }
+
+  template <class Body>
+  static void graph_loop(pode_context* ctx, const IeksSetup<D>& s, Body& body, LoopState* ls, double* trace_dev,
+                         int& it, double& v_prev, const pode_ieks_config& cfg, IeksResult& res) {
+    cudaStream_t st = ctx->stream;
+    LoopState h0{it, 0, cfg.max_iterations, 0, v_prev, cfg.traj_rtol, cfg.obj_atol, cfg.obj_rtol};
+    cuda_check(cudaMemcpyAsync(ls, &h0, sizeof(h0), cudaMemcpyHostToDevice, st), "loop state");
+    reset_error(ctx);
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cuda_check(cudaGraphCreate(&graph, 0), "graph");
+    cudaGraphConditionalHandle h;
+    cuda_check(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault), "cond handle");
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    cuda_check(cudaGraphAddNode(&node, graph, nullptr, 0, &np), "while node");
+    cudaGraph_t g_body = np.conditional.phGraph_out[0];
+    const int64_t l0 = ctx->launches;
+    cuda_check(cudaStreamBeginCaptureToGraph(st, g_body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed),
+               "capture");
+    body(true, h);
+    cuda_check(cudaStreamEndCapture(st, &g_body), "end capture");
+    const int64_t per_iter = ctx->launches - l0;
+    ctx->launches = l0;
+    cuda_check(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
+    cuda_check(cudaGraphLaunch(exec, st), "graph launch");
+    LoopState hs;
+    cuda_check(cudaMemcpyAsync(&hs, ls, sizeof(hs), cudaMemcpyDeviceToHost, st), "loop state");
+    const unsigned long long key = fetch_error(ctx);  // syncs
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    ctx->launches += per_iter * (hs.it - it);
+    std::vector<double> tr(size_t(hs.it), 0.0);
+    if (hs.it > it)
+      cuda_check(cudaMemcpy(tr.data() + it, trace_dev + it, sizeof(double) * (hs.it - it), cudaMemcpyDeviceToHost),
+                 "trace");
+    for (int k = it; k < hs.it; ++k) res.trace.push_back(tr[k]);
+    it = hs.it;
+    v_prev = hs.v_prev;
+    res.converged = hs.converged != 0;
+    if (key != ~0ull) IeksEngine<D>::check_linearization(ctx, s, it);  // throws
+  }
+
+  // Chunk-aggregate scans run on the group engine (engine.cuh): a lane-serial
+  // ⊗_f needs ~250 live doubles per thread and spills.
   static int scan_fanin() {
     const char* env = std::getenv("PODE_SCAN_FANIN");
     const int v = env ? std::atoi(env) : 4;
@@ -121,34 +199,54 @@ struct FastEngine {
 
     IeksResult res;
     int it = 0;
-    while (it < cfg.max_iterations) {
-      ++it;
-      reset_error(ctx);
-      a.eta = eta_a;
-      a.eta_term = term(eta_a);
-      lane::k_lane_fwd_reduce<D, d><<<lblocks, th, 0, st>>>(a, cst, agg);
+    double* const pair0 = eta_a;  // trajectory buffers: iteration i (0-based)
+    double* const pair1 = eta_b;  // linearises at pair[i & 1]
+    LoopState* ls = ws.arr<LoopState>("fast_loop", 1);
+    double* trace_dev = ws.arr<double>("fast_trace", size_t(std::max(1, cfg.max_iterations)));
+    // One iteration's launches.  graph: buffers by device iteration parity
+    // and the stopping rule evaluated on the device (k_finish_iter).
+    auto body = [&](bool graph, cudaGraphConditionalHandle h) {
+      FastArgs ag = a;
+      if (graph) {
+        ag.it_dev = &ls->it;
+        ag.pair0 = pair0;
+        ag.pair1 = pair1;
+        ag.term_off = int64_t(padded) * D;
+      } else {
+        ag.eta = eta_a;
+        ag.eta_term = term(eta_a);
+      }
+      lane::k_lane_fwd_reduce<D, d><<<lblocks, th, 0, st>>>(ag, cst, agg);
       note_launch(ctx, "fast_fwd_reduce");
-      ScanTally tf, tr;
-      if (lane_scans())
-        lane::LaneScan<D, lane::LFOps<D>, false>::run(ctx, agg, agg, nc, 0, scan_fanin(), tf);
-      else
-        tf = Engine<D>::scan_filtering_gauss(ctx, nc, agg, agg, scan_fanin());
-      lane::k_lane_fwd_down<D, d><<<lblocks, th, 0, st>>>(a, cst, agg, soa);
+      const ScanTally tf = Engine<D>::scan_filtering_gauss(ctx, nc, agg, agg, scan_fanin());
+      lane::k_lane_fwd_down<D, d><<<lblocks, th, 0, st>>>(ag, cst, agg, soa);
       note_launch(ctx, "fast_fwd_down");
       lane::k_lane_bfold<D><<<lblocks, th, 0, st>>>(soa, N, L, nc, bagg);
       note_launch(ctx, "fast_bwd_fold");
-      if (lane_scans())
-        lane::LaneScan<D, lane::LMOps<D>, true>::run(ctx, bagg, bagg, nc, 0, scan_fanin(), tr);
-      else
-        tr = Engine<D>::scan_means_terminal(ctx, nc, bagg, scan_fanin());
-      lane::k_lane_bwd_down<D, d, false><<<lblocks, th, 0, st>>>(a, cst, soa, bagg, eta_a, term(eta_a), eta_b,
+      const ScanTally tr = Engine<D>::scan_means_terminal(ctx, nc, bagg, scan_fanin());
+      lane::k_lane_bwd_down<D, d, false><<<lblocks, th, 0, st>>>(ag, cst, soa, bagg, eta_a, term(eta_a), eta_b,
                                                                   term(eta_b), part);
       note_launch(ctx, "fast_bwd_down");
-      finish();
-      IE::check_linearization(ctx, s, it);  // syncs the stream
+      if (graph) {
+        k_finish_iter<<<1, kRedThreads, 0, st>>>(part, nparts, ls, trace_dev, ctx->d_err, h);
+        note_launch(ctx, "finish_iter");
+      } else {
+        finish();
+      }
       // scan tally of the whole time axis: chunk folds + aggregate scans
       res.stats.combines = std::max(res.stats.combines, (N - nc) + tf.combines + N);
       res.stats.depth = std::max(res.stats.depth, int64_t(L) + tf.depth + int64_t(L) + tr.depth);
+    };
+    while (it < cfg.max_iterations) {
+      if (it == 1 && use_graph(ctx, cfg)) {  // workspaces exist after one eager iteration
+        graph_loop(ctx, s, body, ls, trace_dev, it, v_prev, cfg, res);
+        if (res.converged || it >= cfg.max_iterations) break;
+        continue;  // unreachable: the device loop runs to convergence or the budget
+      }
+      ++it;
+      reset_error(ctx);
+      body(false, cudaGraphConditionalHandle{});
+      IE::check_linearization(ctx, s, it);  // syncs the stream
       const double v = 0.5 * ctx->h_scalars[0];
       const double dmax = ctx->h_scalars[1], emax = ctx->h_scalars[2];
       res.trace.push_back(v);
@@ -161,16 +259,63 @@ struct FastEngine {
         break;
       }
     }
+    // newest trajectory in eta_a, final linearisation point in eta_b
+    eta_a = (it & 1) ? pair1 : pair0;
+    eta_b = (it & 1) ? pair0 : pair1;
     res.iterations = it;
-    // row-major copies of the final linearisation point and trajectory
-    double* lin_rows = ws.arr<double>("lane_lin_rows", size_t(n1) * D);
-    double* out_rows = ws.arr<double>("lane_out_rows", size_t(n1) * D);
-    lane::k_eta_rows<D><<<grid1(n1 * D), kRedThreads, 0, st>>>(eta_b, term(eta_b), N, L, nc, lin_rows);
-    note_launch(ctx, "eta_rows");
-    lane::k_eta_rows<D><<<grid1(n1 * D), kRedThreads, 0, st>>>(eta_a, term(eta_a), N, L, nc, out_rows);
-    note_launch(ctx, "eta_rows");
-    IE::finalize(ctx, s, lin_rows, out_rows, cfg.linearization, it, prior.sigma, means, cov, sol_m, sol_c, res);
+    if (std::getenv("PODE_FINALIZE") && std::string(std::getenv("PODE_FINALIZE")) == "elements") {
+      // row-major copies of the final linearisation point and trajectory
+      double* lin_rows = ws.arr<double>("lane_lin_rows", size_t(n1) * D);
+      double* out_rows = ws.arr<double>("lane_out_rows", size_t(n1) * D);
+      lane::k_eta_rows<D><<<grid1(n1 * D), kRedThreads, 0, st>>>(eta_b, term(eta_b), N, L, nc, lin_rows);
+      note_launch(ctx, "eta_rows");
+      lane::k_eta_rows<D><<<grid1(n1 * D), kRedThreads, 0, st>>>(eta_a, term(eta_a), N, L, nc, out_rows);
+      note_launch(ctx, "eta_rows");
+      IE::finalize(ctx, s, lin_rows, out_rows, cfg.linearization, it, prior.sigma, means, cov, sol_m, sol_c, res);
+      return res;
+    }
+    finalize(ctx, s, a, cst, agg, soa, eta_a, term(eta_a), eta_b, term(eta_b), prior.sigma, it,
+             lane::FinOut{means, cov, sol_m, sol_c}, res);
     return res;
+  }
+
+  // Lane finalize at the final linearisation point (the last iteration's
+  // pass-B prefixes in `agg` are still valid for it): F1 filter + C_f(k) +
+  // innovations, F2 chunk smoothing aggregates (E, g, L), a reverse ⊗_s scan
+  // of the aggregates, F4 smoothed factors fused with the outputs.
+  static void finalize(pode_context* ctx, const IeksSetup<D>& s, FastArgs a, const FastConst<D>& cst, const FEd& agg,
+                       const lane::ElemSoA& soa, const double* eta_out, const double* eta_out_term,
+                       const double* eta_lin, const double* eta_lin_term, double sigma, int it,
+                       const lane::FinOut& out, IeksResult& res) {
+    cudaStream_t st = ctx->stream;
+    Workspace& ws = ctx->ws;
+    const int64_t nc = a.nchunks;
+    const size_t padded = size_t(nc) * a.L;
+    double* cf = ws.arr<double>("fin_cf", padded * D * D + D * D);
+    double* cterm = cf + padded * D * D;
+    const unsigned lblocks = static_cast<unsigned>((nc + lane::kLaneThreads - 1) / lane::kLaneThreads);
+    double* part = ws.arr<double>("fin_part", size_t(lblocks) * 3 + 3);
+    double* red = part + size_t(lblocks) * 3;
+    a.eta = eta_lin;
+    a.eta_term = eta_lin_term;
+    reset_error(ctx);
+    lane::k_lane_fwd_down<D, d, true><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, agg, soa, cf, cterm, part);
+    note_launch(ctx, "fin_fwd");
+    k_finish3<<<1, kRedThreads, 0, st>>>(part, lblocks, red);
+    note_launch(ctx, "finish3");
+    IeksEngine<D>::check_linearization(ctx, s, it);  // syncs the stream
+    SEd sagg = Engine<D>::template alloc<SOps<D>>(ctx, "fin_sagg", nc);
+    lane::k_lane_fin_fold<D, d><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, soa, cf, cterm, sagg);
+    note_launch(ctx, "fin_fold");
+    const ScanTally t = Engine<D>::scan_smoothing(ctx, nc, sagg, sagg, true);
+    res.stats.combines = std::max(res.stats.combines, a.N + t.combines);
+    const double count = double(a.N) * s.dim;
+    lane::k_lane_fin_bwd<D, d><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, soa, cf, cterm, sagg, eta_out,
+                                                                       eta_out_term, red, count, out);
+    note_launch(ctx, "fin_bwd");
+    cuda_check(cudaMemcpyAsync(ctx->h_scalars, red, sizeof(double), cudaMemcpyDeviceToHost, st), "innov");
+    IeksEngine<D>::check_linearization(ctx, s, it);  // syncs the stream
+    res.sigma_hat = std::sqrt(ctx->h_scalars[0] / count) * sigma;
   }
 };
 

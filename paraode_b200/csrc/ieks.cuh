@@ -151,8 +151,9 @@ static __global__ void k_eta_objective(const double* smean, const double* scale,
   }
 }
 
-// Fixed-order finish of block partials: out = (sum_0, max_1, max_2).
-static __global__ void k_finish3(const double* part, int64_t nparts, double* out) {
+// Fixed-order finish of block partials (sum_0, max_1, max_2), valid in
+// thread 0 of a kRedThreads block.
+__device__ __forceinline__ void finish3_block(const double* part, int64_t nparts, double (&out)[3]) {
   __shared__ double s0[kRedThreads], s1[kRedThreads], s2[kRedThreads];
   double a = 0.0, b = 0.0, c = 0.0;
   for (int64_t k = threadIdx.x; k < nparts; k += blockDim.x) {
@@ -172,10 +173,18 @@ static __global__ void k_finish3(const double* part, int64_t nparts, double* out
     }
     __syncthreads();
   }
+  out[0] = s0[0];
+  out[1] = s1[0];
+  out[2] = s2[0];
+}
+
+static __global__ void k_finish3(const double* part, int64_t nparts, double* out) {
+  double r[3];
+  finish3_block(part, nparts, r);
   if (threadIdx.x == 0) {
-    out[0] = s0[0];
-    out[1] = s1[0];
-    out[2] = s2[0];
+    out[0] = r[0];
+    out[1] = r[1];
+    out[2] = r[2];
   }
 }
 

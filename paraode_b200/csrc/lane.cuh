@@ -378,6 +378,38 @@ __device__ __forceinline__ void st_mat(double* p, const double (&m)[D][D]) {
     for (int j = 0; j < D; ++j) p[r * D + j] = m[r][j];
 }
 
+// A D x D matrix per node in the chunk-interleaved layout of ElemSoA::e.
+template <int D>
+__device__ __forceinline__ void mat_st(double* base, int64_t nc, int64_t c, int64_t t, const double (&m)[D][D]) {
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int j = 0; j < D; ++j) base[((t * D + r) * D + j) * nc + c] = m[r][j];
+}
+template <int D>
+__device__ __forceinline__ void mat_ld(const double* base, int64_t nc, int64_t c, int64_t t, double (&m)[D][D]) {
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int j = 0; j < D; ++j) m[r][j] = base[((t * D + r) * D + j) * nc + c];
+}
+
+// Block sum of one value per thread (fixed tree order) -> part[3 b] (the
+// k_finish3 partial layout, maxima 0).  Every thread of the block must call it.
+__device__ __forceinline__ void block_sum_partial(double* red, double v, double* part) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int st = kLaneThreads / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[blockIdx.x * 3 + 0] = red[0];
+    part[blockIdx.x * 3 + 1] = 0.0;
+    part[blockIdx.x * 3 + 2] = 0.0;
+  }
+}
+
 // ------------------------------------------------------------- pass A ---
 // One thread per chunk: fold the chunk's filtering elements into the
 // aggregate (A, b, C, eta, J) (see fast.cuh for the algebra).
@@ -387,6 +419,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(FastArgs a, Fa
   constexpr int B = M::B;
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (c >= a.nchunks) return;
+  resolve_lin(a);
   const int64_t s = c * a.L;
   const int64_t e = min(a.N, s + a.L);
   double A[D][D], C[D][D], J[D][D], b[D], eta[D];
@@ -505,13 +538,17 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(FastArgs a, Fa
 // One thread per chunk: square-root Kalman filter from the chunk's incoming
 // filtered marginal; smoothing elements E_n, g_n (parallel.cpp:112-135) of
 // every node (chunk-interleaved layout, ElemSoA).
-template <int D, int d>
-__global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, FastConst<D> cst, FEd prefix,
-                                                                ElemSoA elems) {
+// kFinal (once, after convergence): also stores the filtered factor C_f(k)
+// of every node (cf, chunk-interleaved like E; node N in cterm) and reduces
+// the whitened innovations ||S^-1 (H m- - offset)||^2 (innovation_stats,
+// ieks.cpp:79-104) into one partial per block.
+template <int D, int d, bool kFinal>
+__device__ __forceinline__ double fwd_down_chunk(FastArgs a, const FastConst<D>& cst, const FEd& prefix,
+                                                 const ElemSoA& elems, double* cf, double* cterm, int64_t c) {
   using M = Model<D, d>;
   constexpr int B = M::B;
-  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (c >= a.nchunks) return;
+  double innov = 0.0;
+  resolve_lin(a);
   const int64_t s = c * a.L;
   const int64_t e = min(a.N, s + a.L);
   double m[D], C[D][D];
@@ -538,6 +575,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
     for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
     M::phi_coefs(ratio, pc);
     // Y = C (phi C)^T = C C^T phi^T; C- = tria([phi C, Q]); E = Y C-^-T C-^-1
+    if constexpr (kFinal) mat_st<D>(cf, a.nchunks, c, k - s, C);
     double pcC[D][D];
 #pragma unroll
     for (int r = 0; r < D; ++r)
@@ -602,10 +640,18 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
     double z[d];
     M::h_vec(lin, tn, mm, z);
 #pragma unroll
+    for (int i = 0; i < d; ++i) z[i] -= lin.off[i];
+    if constexpr (kFinal) {
+      double w[d];
+      M::s_solve(u, z, w);
+#pragma unroll
+      for (int i = 0; i < d; ++i) innov = fma(w[i], w[i], innov);
+    }
+#pragma unroll
     for (int r = 0; r < D; ++r) {
       double v = mm[r];
 #pragma unroll
-      for (int i = 0; i < d; ++i) v = fma(-u.k[r][i], z[i] - lin.off[i], v);
+      for (int i = 0; i < d; ++i) v = fma(-u.k[r][i], z[i], v);
       m[r] = v;
 #pragma unroll
       for (int j = 0; j < D; ++j) C[r][j] = (j <= r) ? cm[r][j] : 0.0;
@@ -619,9 +665,22 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
   if (e == a.N) {  // terminal node N: E = 0, g = m_f(N) (parallel.cpp:137-144)
 #pragma unroll
     for (int r = 0; r < D; ++r) elems.term[r] = m[r];
+    if constexpr (kFinal) st_mat<D>(cterm, C);
   }
   if (bad_lin >= 0) raise_error(a.err, bad_lin, kErrLinearization);
   if (bad_sing) raise_error(a.err, s, kErrSingular);
+  return innov;
+}
+
+template <int D, int d, bool kFinal = false>
+__global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, FastConst<D> cst, FEd prefix,
+                                                                ElemSoA elems, double* cf = nullptr,
+                                                                double* cterm = nullptr, double* part = nullptr) {
+  __shared__ double red[kFinal ? kLaneThreads : 1];
+  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  double innov = 0.0;
+  if (c < a.nchunks) innov = fwd_down_chunk<D, d, kFinal>(a, cst, prefix, elems, cf, cterm, c);
+  if constexpr (kFinal) block_sum_partial(red, innov, part);  // every thread reaches the barriers
 }
 
 // Pass C2: one thread per chunk folds the chunk's smoothing elements in time
@@ -672,6 +731,222 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_bfold(ElemSoA elems, int6
   for (int r = 0; r < D; ++r) bagg.g[c * D + r] = gg[r];
 }
 
+// ------------------------------------------------- finalize (once) ---
+// Smoothing-element covariance factor in Joseph form,
+//   L_k = tria([(I - E_k phi_k) C_f(k), E_k Q^1/2]),
+// L L^T = P_f - E P^- E^T: the same Gaussian as the lower-right block of the
+// reference's tria (make_smoothing_element, parallel.cpp:112-135).
+template <int D, int d>
+__device__ __forceinline__ void smooth_factor(const double (&pc)[D / d][D / d], const double (&E)[D][D],
+                                              const double (&cf)[D][D], const double* q, double (&lk)[D][D]) {
+  using M = Model<D, d>;
+  double x[D][D];
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int j = 0; j < D; ++j) x[r][j] = cf[r][j];
+  M::template phi_rows<D>(pc, x);
+  double m[D][2 * D];
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double acc = cf[r][j], acq = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        acc = fma(-E[r][k], x[k][j], acc);
+        if (k >= j) acq = fma(E[r][k], q[k * D + j], acq);  // Q^1/2 lower triangular
+      }
+      m[r][j] = acc;
+      m[r][D + j] = acq;
+    }
+  lq<D, 2 * D, D>(m);
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int j = 0; j < D; ++j) lk[r][j] = (j <= r) ? m[r][j] : 0.0;
+}
+
+// l <- tria([E l, lk]) (⊗_s covariance part, parallel.cpp:146-156; lk lower).
+template <int D>
+__device__ __forceinline__ void smooth_combine_factor(const double (&E)[D][D], const double (&lk)[D][D],
+                                                      double (&l)[D][D]) {
+  double m[D][2 * D];
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) acc = fma(E[r][k], l[k][j], acc);
+      m[r][j] = acc;
+      m[r][D + j] = lk[r][j];
+    }
+  lq<D, 2 * D, D, D>(m);
+#pragma unroll
+  for (int r = 0; r < D; ++r)
+#pragma unroll
+    for (int j = 0; j < D; ++j) l[r][j] = (j <= r) ? m[r][j] : 0.0;
+}
+
+// F2: each chunk's full smoothing aggregate e_s ⊗ .. ⊗ e_{e-1} (⊗ the
+// terminal element for the last chunk) as (E, g, L), folded backwards; the
+// per-node L_k are formed on the fly from (E_k, C_f(k)).
+template <int D, int d>
+__global__ void __launch_bounds__(kLaneThreads) k_lane_fin_fold(FastArgs a, FastConst<D> cst, ElemSoA elems,
+                                                                const double* cf, const double* cterm, SEd agg) {
+  using M = Model<D, d>;
+  constexpr int B = M::B;
+  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (c >= a.nchunks) return;
+  const int64_t s = c * a.L;
+  const int64_t e = min(a.N, s + a.L);
+  const bool last = c == a.nchunks - 1;
+  double ea[D][D], la[D][D], ga[D];
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    ga[r] = last ? elems.term[r] : 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      ea[r][j] = (!last && r == j) ? 1.0 : 0.0;
+      la[r][j] = last ? cterm[r * D + j] : 0.0;
+    }
+  }
+  double tn[B], tni[B];
+  M::taus(a.grid, e, tn, tni);
+  for (int64_t k = e - 1; k >= s; --k) {
+    double tk[B], tki[B], ratio[B], pc[B][B];
+    M::taus(a.grid, k, tk, tki);
+#pragma unroll
+    for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
+    M::phi_coefs(ratio, pc);
+    double E[D][D], gk[D], cfk[D][D], lk[D][D];
+    soa_ld<D>(elems, c, k - s, E, gk);
+    mat_ld<D>(cf, a.nchunks, c, k - s, cfk);
+    smooth_factor<D, d>(pc, E, cfk, cst.q, lk);
+    smooth_combine_factor<D>(E, lk, la);
+    double ne[D][D], ng[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      double acc = gk[r];
+#pragma unroll
+      for (int x = 0; x < D; ++x) acc = fma(E[r][x], ga[x], acc);
+      ng[r] = acc;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double v = 0.0;
+#pragma unroll
+        for (int x = 0; x < D; ++x) v = fma(E[r][x], ea[x][j], v);
+        ne[r][j] = v;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      ga[r] = ng[r];
+#pragma unroll
+      for (int j = 0; j < D; ++j) ea[r][j] = ne[r][j];
+    }
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      tn[i] = tk[i];
+      tni[i] = tki[i];
+    }
+  }
+  st_mat<D>(agg.e + c * D * D, ea);
+  st_mat<D>(agg.l + c * D * D, la);
+#pragma unroll
+  for (int r = 0; r < D; ++r) agg.g[c * D + r] = ga[r];
+}
+
+// Calibrated outputs of node n (ieks.cpp:196-208): means = eta, cov_sqrt =
+// T_n L^s_n sigma_rel, and their solution-component projections.
+struct FinOut {
+  double* means;
+  double* cov;
+  double* sol_m;
+  double* sol_c;
+};
+
+template <int D, int d>
+__device__ __forceinline__ void write_node(const FinOut& o, int64_t n, const double (&t)[D / d],
+                                           const double (&ls)[D][D], const double (&eta)[D], double sig) {
+  constexpr int B = D / d;
+  if (o.means) {
+#pragma unroll
+    for (int r = 0; r < D; ++r) o.means[n * D + r] = eta[r];
+  }
+  if (o.cov) {
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int j = 0; j < D; ++j) o.cov[(n * D + r) * D + j] = t[r % B] * ls[r][j] * sig;
+  }
+  if (o.sol_m) {
+#pragma unroll
+    for (int i = 0; i < d; ++i) o.sol_m[n * d + i] = eta[i * B];
+  }
+  if (o.sol_c) {
+#pragma unroll
+    for (int i = 0; i < d; ++i)
+#pragma unroll
+      for (int j = 0; j < d; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc += (t[0] * ls[i * B][k] * sig) * (t[0] * ls[j * B][k] * sig);
+        o.sol_c[(n * d + i) * d + j] = acc;
+      }
+  }
+}
+
+// F4: backward smoothed-factor recursion L^s_k = tria([E_k L^s_{k+1}, L_k])
+// from each chunk's incoming factor (the reverse scan of the F2 aggregates;
+// the last chunk starts from C_f(N)), fused with the output projection.
+template <int D, int d>
+__global__ void __launch_bounds__(kLaneThreads) k_lane_fin_bwd(FastArgs a, FastConst<D> cst, ElemSoA elems,
+                                                               const double* cf, const double* cterm, SEd suffix,
+                                                               const double* eta_out, const double* eta_out_term,
+                                                               const double* innov, double count, FinOut o) {
+  using M = Model<D, d>;
+  constexpr int B = M::B;
+  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (c >= a.nchunks) return;
+  const int64_t s = c * a.L;
+  const int64_t e = min(a.N, s + a.L);
+  const bool last = c == a.nchunks - 1;
+  const double sig = sqrt(innov[0] / count);
+  double ls[D][D];
+  ld_mat<D>(last ? cterm : suffix.l + (c + 1) * D * D, ls);
+  double tn[B], tni[B];
+  M::taus(a.grid, e, tn, tni);
+  if (last) {
+    double eta[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) eta[r] = eta_out_term[r];
+    write_node<D, d>(o, e, tn, ls, eta, sig);
+  }
+  for (int64_t k = e - 1; k >= s; --k) {
+    double tk[B], tki[B], ratio[B], pc[B][B];
+    M::taus(a.grid, k, tk, tki);
+#pragma unroll
+    for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
+    M::phi_coefs(ratio, pc);
+    double E[D][D], gk[D], cfk[D][D], lk[D][D];
+    soa_ld<D>(elems, c, k - s, E, gk);
+    mat_ld<D>(cf, a.nchunks, c, k - s, cfk);
+    smooth_factor<D, d>(pc, E, cfk, cst.q, lk);
+    smooth_combine_factor<D>(E, lk, ls);
+    double eta[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r) eta[r] = eta_out[((k - s) * D + r) * a.nchunks + c];
+    write_node<D, d>(o, k, tk, ls, eta, sig);
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      tn[i] = tk[i];
+      tni[i] = tki[i];
+    }
+  }
+}
+
 // ------------------------------------------------------------- pass E ---
 // One thread per chunk: backward mean recursion m_n = g_n + E_n m_{n+1}
 // from the chunk's incoming smoothed mean; new trajectory (original
@@ -691,6 +966,13 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, Fast
   const bool okc = c < a.nchunks;
   const int64_t nc = a.nchunks;
   double obj = 0.0, dmax = 0.0, emax = 0.0;
+  if (a.it_dev != nullptr) {  // graph-loop mode: buffers by iteration parity
+    const int par = *a.it_dev & 1;
+    eta_old = par ? a.pair1 : a.pair0;
+    old_term = eta_old + a.term_off;
+    eta_new = par ? a.pair0 : a.pair1;
+    new_term = eta_new + a.term_off;
+  }
   if (okc) {
     const int64_t s = c * a.L;
     const int64_t e = min(a.N, s + a.L);

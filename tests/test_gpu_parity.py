@@ -220,11 +220,13 @@ def test_para_ieks_matches_seq_ieks(name, nu, steps):  # acceptance.cpp:97-123 (
     assert rel(dense_cov(got.cov_sqrt), dense_cov(want["cov_sqrt"])) <= 1e-7
     assert got.sigma_hat == pytest.approx(want["sigma_hat"], rel=1e-7)
     assert rel(got.solution_means, want["solution_means"]) <= 1e-9
+    assert rel(got.solution_covs, want["solution_covs"]) <= 1e-7
     assert np.allclose(got.objective_trace, want["objective_trace"], rtol=1e-8, atol=1e-12)
 
 
 @pytest.mark.parametrize("chunk,fanin", [(2, 2), (3, 2), (5, 3), (8, 4), (7, 16), (30, 4), (64, 2)])
-@pytest.mark.parametrize("name,nu,steps", [("logistic", 2, 30), ("vanderpol", 2, 100), ("fhn", 2, 257)])
+@pytest.mark.parametrize("name,nu,steps", [("logistic", 2, 30), ("vanderpol", 2, 100), ("fhn", 2, 257),
+                                           ("fhn", 2, 4000), ("rigidbody", 2, 3000)])
 def test_fused_engine_chunking(monkeypatch, name, nu, steps, chunk, fanin):
     """Fused IEKS engine under every chunking shape: one chunk, ragged last
     chunks, single- and multi-level aggregate scans (top level of 1..fanin
@@ -238,6 +240,22 @@ def test_fused_engine_chunking(monkeypatch, name, nu, steps, chunk, fanin):
     assert got.iterations == want["iterations"]
     assert rel(got.means, want["means"]) <= 1e-9
     assert rel(got.solution_means, want["solution_means"]) <= 1e-9
+
+
+@pytest.mark.parametrize("env", [{"PODE_BSCAN": "0"}, {"PODE_FINALIZE": "elements"}, {}])
+def test_fused_engine_variants(monkeypatch, env):
+    """The alternative scan / finalize paths of the fused engine agree with the oracle too."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    monkeypatch.setenv("PODE_CHUNK", "3")
+    op = O.problem("fhn")
+    grid = O.uniform_grid(op.t_end, 2000)
+    want = O.ieks(op, 2, grid, mode=0)
+    got = P.para_ieks(P.problem_by_name("fhn"), P.IwpPrior(2, op.dim, 1.0), grid)
+    assert got.iterations == want["iterations"]
+    assert rel(got.means, want["means"]) <= 1e-9
+    assert rel(dense_cov(got.cov_sqrt), dense_cov(want["cov_sqrt"])) <= 1e-7
+    assert got.sigma_hat == pytest.approx(want["sigma_hat"], rel=1e-7)
 
 
 def test_logistic_frozen_rmse():  # acceptance.cpp:167-179 — reference measured 1.374e-6, gate 2.1e-6
