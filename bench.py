@@ -131,6 +131,14 @@ def scan_model(N, D, sm=148, fanin=4):
     n = -(-nc // fanin)
     downs = [(nc, fanin)] if n > 1 else []
     while n > 1:
+        if n > 4096:  # engine.cuh bscan_max(): large levels stay sequential fan-in
+            m = -(-n // fanin)
+            add("scan_g_reduce", (n - m) * f_full, 2 * n * el_f)
+            add("scan_m_reduce", (n - m) * f_aff, 2 * n * el_m)
+            if m > 1:
+                downs.append((n, fanin))
+            n = m
+            continue
         nb = -(-n // G)
         work = sum(sklansky_readers(min(G, n - b * G)) for b in range(nb))
         add("bscan_g", work * f_full, 2 * n * el_f)

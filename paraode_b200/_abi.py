@@ -3,7 +3,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libparaode_b200.so")
+LIB_PATH = os.environ.get("PODE_LIB") or os.path.join(_HERE, "_lib", "libparaode_b200.so")
 
 dptr = C.POINTER(C.c_double)
 iptr = C.POINTER(C.c_int32)

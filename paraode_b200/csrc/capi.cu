@@ -172,7 +172,10 @@ template <typename T>
 void stage_out(pode_context* ctx, T* dst, const T* dev, size_t count, bool device) {
   if (dst == nullptr || device) return;
   const size_t bytes = sizeof(T) * count;
-  if (bytes >= (size_t(4) << 20)) {
+  cudaPointerAttributes attr{};
+  const bool pinned = cudaPointerGetAttributes(&attr, dst) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // clear a failed query on plain pageable memory
+  if (!pinned && bytes >= (size_t(4) << 20)) {
     copy_out_staged(ctx, reinterpret_cast<char*>(dst), reinterpret_cast<const char*>(dev), bytes);
     return;
   }

@@ -363,11 +363,19 @@ __global__ void __launch_bounds__(kThreads) k_scan_down(typename Op::Arr x, int6
   if (okc && g.r == 0 && bad) raise_error(err, lo, kErrSingular);
 }
 
+// The aggregate-scan kernels are latency-bound per group: cap them at 168
+// registers (3 blocks of 4 warps per SM; measured 1 / 3 / 4: 3 is best, 4
+// spills the block scan).
+#ifndef PODE_GROUP_MIN_BLOCKS
+#define PODE_GROUP_MIN_BLOCKS 3
+#endif
+constexpr int kGroupMinBlocks = PODE_GROUP_MIN_BLOCKS;
+
 // --------------------------------------------- Gaussian-carry ⊗_f scan ---
 // Reduce that also keeps every chunk-local inclusive prefix (loc), so the
 // down-sweep is ONE combine deep: out[k] = carry ⊗ loc[k], independent k.
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_scan_reduce_loc(FEd x, int64_t n, int L, FEd loc, FEd agg,
+__global__ void __launch_bounds__(kThreads, kGroupMinBlocks) k_scan_reduce_loc(FEd x, int64_t n, int L, FEd loc, FEd agg,
                                                               DevError* err) {
   extern __shared__ double smem[];
   const Grp<D> g = make_group<D>(smem);
@@ -395,7 +403,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_reduce_loc(FEd x, int64_t n, 
 
 // out[k] (b, C only) = carry[k / L - 1] ⊗ loc[k]; chunk 0 copies loc.
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_scan_down_gauss(FEd loc, int64_t n, int L, FEd carry, FEd out,
+__global__ void __launch_bounds__(kThreads, kGroupMinBlocks) k_scan_down_gauss(FEd loc, int64_t n, int L, FEd carry, FEd out,
                                                               DevError* err) {
   extern __shared__ double smem[];
   const Grp<D> g = make_group<D>(smem);
@@ -487,13 +495,17 @@ constexpr size_t bscan_smem() {
 }
 
 template <int D, class Op, bool kRev>
-__global__ void __launch_bounds__(kBWarps * 32) k_bscan_loc(typename Op::Arr x, int64_t n, typename Op::Arr loc,
+__global__ void __launch_bounds__(kBWarps * 32, kGroupMinBlocks / 2) k_bscan_loc(typename Op::Arr x, int64_t n, typename Op::Arr loc,
                                                             typename Op::Arr agg, DevError* err) {
   extern __shared__ double smem[];
   constexpr int G = bscan_groups<D>();
   const Grp<D> g = make_group<D>(smem);
   const typename Op::Arr sb = Op::smem_arr(smem + kBWarps * Grp<D>::kSlots * Scratch<D>::kDoubles, G);
-  const int p = (threadIdx.x >> 5) * Grp<D>::kPerWarp + g.gw;  // position in the block
+  // position in the block, warp index in the low bits: the Sklansky steps
+  // h < kBWarps then split readers / idle groups along whole warps, and an
+  // idle warp skips its combine
+  const int warp = threadIdx.x >> 5;
+  const int p = g.gw * kBWarps + warp;
   const bool real = g.real();
   const int64_t lo = int64_t(blockIdx.x) * G;
   const int64_t hi = min(n, lo + G);
@@ -508,22 +520,28 @@ __global__ void __launch_bounds__(kBWarps * 32) k_bscan_loc(typename Op::Arr x, 
     if (real && (p & (2 * h - 1)) == h - 1) Op::store(sb, p, g.r, true, acc);
     __syncthreads();
     const bool rd = real && (p & h);
-    const int j = (p & ~(2 * h - 1)) + h - 1;
-    const auto left = Op::load(sb, rd ? j : 0, g.r, rd);
-    typename Op::El tmp;
-    const bool good = kRev ? Op::combine(g, acc, left, tmp) : Op::combine(g, left, acc, tmp);
-    bad |= rd && ok && !good;
-    acc = Op::select(rd, tmp, acc);
+    if (h >= kBWarps || (warp & h)) {  // warp-uniform
+      const int j = (p & ~(2 * h - 1)) + h - 1;
+      const auto left = Op::load(sb, rd ? j : 0, g.r, rd);
+      typename Op::El tmp;
+      const bool good = kRev ? Op::combine(g, acc, left, tmp) : Op::combine(g, left, acc, tmp);
+      bad |= rd && ok && !good;
+      acc = Op::select(rd, tmp, acc);
+    }
   }
   Op::store(loc, k, g.r, ok, acc);
   if (ok && p == cnt - 1) Op::store(agg, blockIdx.x, g.r, true, acc);
   if (ok && g.r == 0 && bad) raise_error(err, k, kErrSingular);
 }
 
-// Upper scan levels use the block kernel unless PODE_BSCAN=0.
-inline bool use_bscan() {
+// Scan levels above 0 with at most this many elements use the block kernel
+// (latency-bound: Sklansky depth); larger levels keep the work-efficient
+// sequential fan-in (throughput-bound).  PODE_BSCAN=0 disables, =n sets it.
+inline int64_t bscan_max() {
   const char* env = std::getenv("PODE_BSCAN");
-  return env == nullptr || std::atoi(env) != 0;
+  if (env == nullptr) return 4096;
+  const long long v = std::atoll(env);
+  return v == 1 ? (int64_t(1) << 62) : int64_t(v);
 }
 
 // ------------------------------------------------------------- engine ---
@@ -598,7 +616,7 @@ struct Engine {
     DevError* err = reinterpret_cast<DevError*>(ctx->d_err);
     size_t sm = smem_bytes<D>();
     FEd loc = alloc<FOps<D>>(ctx, "gscan_loc_" + std::to_string(level), n);
-    if (level >= 1 && use_bscan()) {  // block Sklansky levels
+    if (level >= 1 && n <= bscan_max()) {  // block Sklansky levels
       constexpr int G = bscan_groups<D>();
       sm = bscan_smem<D, FOps<D>>();
       static bool attr = false;
@@ -671,7 +689,7 @@ struct Engine {
   static void mscan_rec(pode_context* ctx, SEd in, SEd out, int64_t n, int level, int L, ScanTally& t) {
     size_t sm = smem_bytes<D>();
     SEd loc = alloc<SOps<D>>(ctx, "mscan_loc_" + std::to_string(level), n);
-    if (level >= 1 && use_bscan()) {  // block Sklansky levels
+    if (level >= 1 && n <= bscan_max()) {  // block Sklansky levels
       constexpr int G = bscan_groups<D>();
       sm = bscan_smem<D, MOps<D>>();
       static bool attr = false;

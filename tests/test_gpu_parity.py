@@ -242,7 +242,8 @@ def test_fused_engine_chunking(monkeypatch, name, nu, steps, chunk, fanin):
     assert rel(got.solution_means, want["solution_means"]) <= 1e-9
 
 
-@pytest.mark.parametrize("env", [{"PODE_BSCAN": "0"}, {"PODE_FINALIZE": "elements"}, {}])
+@pytest.mark.parametrize("env", [{"PODE_BSCAN": "0"}, {"PODE_BSCAN": "1"}, {"PODE_BSCAN": "64"},
+                                 {"PODE_FINALIZE": "elements"}, {"PODE_GRAPH": "0"}, {}])
 def test_fused_engine_variants(monkeypatch, env):
     """The alternative scan / finalize paths of the fused engine agree with the oracle too."""
     for k, v in env.items():
