@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--problem", default="fhn")
     ap.add_argument("--nu", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="auto", choices=["auto", "shard", "replicas"],
+                    help="N>1: shard one solve along time (strong scaling, default) or run replicas")
     return ap.parse_args()
 
 
@@ -237,7 +239,11 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("PODE_BENCH_BACKEND", "nccl")  # gloo: functional runs of N ranks on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     import ctypes as C
 
@@ -251,13 +257,16 @@ def run_ours(args):
     D, d = prob.dim * (nu + 1), prob.dim
     grid = P.uniform_grid(prob.t_end, n)
     n1 = n + 1
+    shard = world > 1 and args.mode != "replicas"
+    rows = P.shard_range(n1, rank, world)[1] if shard else n1
     dev = torch.device("cuda", local)
-    out_dev = [torch.empty((n1, D), dtype=torch.float64, device=dev),
-               torch.empty((n1, D, D), dtype=torch.float64, device=dev),
-               torch.empty((n1, d), dtype=torch.float64, device=dev),
-               torch.empty((n1, d, d), dtype=torch.float64, device=dev)]
+    out_dev = [torch.empty((rows, D), dtype=torch.float64, device=dev),
+               torch.empty((rows, D, D), dtype=torch.float64, device=dev),
+               torch.empty((rows, d), dtype=torch.float64, device=dev),
+               torch.empty((rows, d, d), dtype=torch.float64, device=dev)]
     grid_pinned = torch.from_numpy(grid).pin_memory()
     cfg = P.IeksConfig()
+    gather = P.torch_allgather() if shard else None
 
     def solve_device():
         ptr = [C.cast(C.c_void_p(t.data_ptr()), A.dptr) for t in out_dev]
@@ -268,13 +277,23 @@ def run_ours(args):
         prior = A.Prior(nu, d, 1.0)
         c = A.IeksConfig(cfg.max_iterations, cfg.traj_rtol, cfg.obj_atol, cfg.obj_rtol, 0)
         st = A.Status()
-        rc = ctx._lib.pode_ieks(ctx.handle, C.byref(pr), C.byref(prior),
-                                C.cast(C.c_void_p(grid_pinned.data_ptr()), A.dptr), n1, C.byref(c),
-                                C.byref(rep), C.byref(st))
+        gp = C.cast(C.c_void_p(grid_pinned.data_ptr()), A.dptr)
+        if shard:
+            comm, failure = P.api.make_shard_comm(rank, world, gather)
+            rc = ctx._lib.pode_ieks_sharded(ctx.handle, C.byref(pr), C.byref(prior), gp, n1, C.byref(c),
+                                            C.byref(comm), C.byref(rep), C.byref(st))
+            if failure:
+                raise failure[0]
+        else:
+            rc = ctx._lib.pode_ieks(ctx.handle, C.byref(pr), C.byref(prior), gp, n1, C.byref(c),
+                                    C.byref(rep), C.byref(st))
         P.api._raise(rc, st)
         return rep
 
     def solve_public():
+        if shard:
+            return P.para_ieks_sharded(prob, P.IwpPrior(nu, d, 1.0), grid, rank, world, gather, cfg,
+                                       want_cov=True, ctx=ctx)
         return P.para_ieks(prob, P.IwpPrior(nu, d, 1.0), grid, cfg, want_cov=True, ctx=ctx)
 
     for _ in range(args.warmup):
@@ -318,9 +337,10 @@ def run_ours(args):
         # above)
         ms_prof, _, prof = timed(solve_device, profile=True)
     ms_e2e, _, _ = timed(solve_public)
-    value = world * n / (ms * 1e-3)
-    e2e = world * n / (ms_e2e * 1e-3)
-    d2h = n1 * (D + D * D + d + d * d) * 8
+    units = n if shard else world * n  # sharded: one solve of n steps over all ranks
+    value = units / (ms * 1e-3)
+    e2e = units / (ms_e2e * 1e-3)
+    d2h = rows * (D + D * D + d + d * d) * 8  # this rank's report rows
     h2d = n1 * 8
     if rank != 0:
         return
@@ -330,15 +350,16 @@ def run_ours(args):
     # timed region (lane passes: per-step counts x N x iterations; scan trees:
     # per-iteration tree counts x iterations) / its summed event time.
     hbm, hbm_src, fp64, fp64_src = peaks()
+    n_loc = (rows - (1 if rank == world - 1 else 0)) if shard else n  # steps this rank processed
     per_step = kernel_model(D, d)
-    per_iter = scan_model(n, D)
+    per_iter = scan_model(n_loc, D)
     total_ms = sum(v[1] for v in prof.values())
     solves = args.steps
 
     def work(name):
         if name in per_step:
             fl, by = per_step[name]
-            return fl * n * iters * solves, by * n * iters * solves
+            return fl * n_loc * iters * solves, by * n_loc * iters * solves
         if name in per_iter:
             fl, by = per_iter[name]
             return fl * iters * solves, by * iters * solves
@@ -378,12 +399,15 @@ def run_ours(args):
                 for k, _ in ranked}
     kernels = {k: {"launches": c, "ms_per_step": t / args.steps} for k, (c, t) in sorted(prof.items())}
     line = {"metric": METRIC, "value": value, "unit": "time-steps/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{prob.name} d={d} IWP(q={nu}) D={D}, N=2^{args.log2n} uniform steps, "
                                    "IEKS to the reference stopping rule", "N": n, "iterations": iters,
                        "converged": converged, "step_iterations_per_s": value * iters / world,
-                       "parallelism": f"replicas x{world}", "l2": "working set > L2 (126 MB) per solve"},
+                       "parallelism": f"time-axis shards x{world} (gloo/nccl all-gather of chunk aggregates)"
+                                      if shard else f"replicas x{world}",
+                       "l2": "working set > L2 (126 MB) per solve"},
             "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof,
             "e2e": {"value": e2e, "unit": "time-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "kernels": kernels, "roofline_top_kernels": roof_all, "ms_per_step_profiled": ms_prof}

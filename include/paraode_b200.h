@@ -225,6 +225,39 @@ int pode_ieks(pode_context* ctx, const pode_problem* problem, const pode_prior* 
               const double* grid, int64_t n_nodes, const pode_ieks_config* config,
               pode_ieks_report* report, pode_status* status);
 
+/* ---- time-axis sharding (one process per GPU) ----------
+ * The reference has no multi-device path; this is the SURVEY.md §8(e)
+ * partition of the same solve.  Shard r of R owns steps [s_r, e_r),
+ * s_r = floor(N r / R), and reports nodes s_r .. e_r - 1 (the last shard
+ * also node N).  Per iteration the shards exchange, through the caller's
+ * all-gather: the forward aggregate of their steps (3D^2+2D doubles), the
+ * backward mean aggregate (D^2+D) and the three stopping scalars; the
+ * finalize exchanges the innovation sum and the smoothing aggregate
+ * (2D^2+D).  Every fold of exchanged values runs in rank order on the
+ * device, so all shards take identical stopping decisions. */
+
+/* All-gather of `count` doubles from every rank into recv[rank * count + i]
+ * (host memory).  Returns 0 on success. */
+typedef int (*pode_allgather_fn)(void* user, const double* send, int64_t count, double* recv);
+
+typedef struct {
+  int32_t rank;
+  int32_t ranks;
+  pode_allgather_fn allgather;
+  void* user;
+} pode_shard_comm;
+
+/* Shard node range of `rank` (first node, number of reported nodes). */
+void pode_shard_range(int64_t n_nodes, int32_t rank, int32_t ranks, int64_t* first_node, int64_t* count);
+
+/* para_ieks over a time-axis shard: `grid` is the GLOBAL grid (n_nodes);
+ * the report arrays hold this shard's nodes (pode_shard_range), the scalars
+ * (iterations, converged, sigma_hat, objective trace) are global.  Requires
+ * an ODE information operator the fused engine serves (d <= 3, D <= 9). */
+int pode_ieks_sharded(pode_context* ctx, const pode_problem* problem, const pode_prior* prior,
+                      const double* grid, int64_t n_nodes, const pode_ieks_config* config,
+                      const pode_shard_comm* comm, pode_ieks_report* report, pode_status* status);
+
 #ifdef __cplusplus
 }
 #endif

@@ -61,6 +61,14 @@ class IeksReport(C.Structure):
                 ("sigma_hat", C.c_double), ("scan_stats", ScanStats)]
 
 
+# int (*)(void* user, const double* send, int64_t count, double* recv)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, dptr, C.c_int64, dptr)
+
+
+class ShardComm(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("ranks", C.c_int32), ("allgather", ALLGATHER_FN), ("user", C.c_void_p)]
+
+
 SYMBOLS = {
     "pode_context_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p), C.POINTER(Status)]),
     "pode_context_destroy": (None, [C.c_void_p]),
@@ -89,6 +97,10 @@ SYMBOLS = {
                            C.POINTER(Status)]),
     "pode_ieks": (C.c_int, [C.c_void_p, C.POINTER(Problem), C.POINTER(Prior), dptr, C.c_int64,
                             C.POINTER(IeksConfig), C.POINTER(IeksReport), C.POINTER(Status)]),
+    "pode_shard_range": (None, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "pode_ieks_sharded": (C.c_int, [C.c_void_p, C.POINTER(Problem), C.POINTER(Prior), dptr, C.c_int64,
+                                    C.POINTER(IeksConfig), C.POINTER(ShardComm), C.POINTER(IeksReport),
+                                    C.POINTER(Status)]),
 }
 
 _lib = None

@@ -485,3 +485,98 @@ def para_ieks(ivp: InitialValueProblem, prior: IwpPrior, grid: Sequence[float],
     return SolverReport(grid.copy(), means, cov, sm, sc, rep.sigma_hat, rep.iterations,
                         trace[:rep.iterations].copy(), bool(rep.converged),
                         rep.scan_stats.combine_invocations, rep.scan_stats.sequential_depth)
+
+
+# ------------------------------------------------ time-axis sharding ---
+def shard_range(n_nodes: int, rank: int, ranks: int):
+    """(first node, reported node count) of shard `rank` (pode_shard_range)."""
+    lo, cnt = C.c_int64(), C.c_int64()
+    A.load().pode_shard_range(n_nodes, rank, ranks, C.byref(lo), C.byref(cnt))
+    return lo.value, cnt.value
+
+
+def torch_allgather(group=None):
+    """All-gather adapter over torch.distributed for para_ieks_sharded: gloo
+    gathers host tensors; nccl gathers on the current CUDA device."""
+    import torch
+    import torch.distributed as dist
+
+    def gather(send: np.ndarray) -> np.ndarray:
+        ranks = dist.get_world_size(group)
+        t = torch.from_numpy(np.ascontiguousarray(send))
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        out = torch.empty(ranks * t.numel(), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t, group=group)
+        return out.cpu().numpy()
+    return gather
+
+
+def make_shard_comm(rank: int, ranks: int, allgather):
+    """pode_shard_comm for a Python all-gather (send ndarray -> rank-ordered
+    ndarray).  Returns (comm, failures); keep comm alive during the call."""
+    failure = []
+
+    def cb(_user, send, count, recv):
+        try:
+            snd = np.ctypeslib.as_array(send, shape=(count,)).copy()
+            got = np.asarray(allgather(snd), dtype=np.float64).reshape(-1)
+            if got.shape[0] != count * ranks:
+                raise ValueError(f"all-gather returned {got.shape[0]} values, want {count * ranks}")
+            np.ctypeslib.as_array(recv, shape=(count * ranks,))[:] = got
+            return 0
+        except Exception as e:  # reported through the ABI as a failed exchange
+            failure.append(e)
+            return 1
+
+    comm = A.ShardComm(rank, ranks, A.ALLGATHER_FN(cb), None)
+    comm._keep = cb
+    return comm, failure
+
+
+@dataclass
+class ShardReport:
+    """This shard's part of a SolverReport: nodes first_node .. first_node +
+    means.shape[0] - 1; the scalars are those of the whole solve."""
+    first_node: int
+    times: np.ndarray
+    means: np.ndarray
+    cov_sqrt: Optional[np.ndarray]
+    solution_means: np.ndarray
+    solution_covs: Optional[np.ndarray]
+    sigma_hat: float
+    iterations: int
+    objective_trace: np.ndarray
+    converged: bool
+
+
+def para_ieks_sharded(ivp: InitialValueProblem, prior: IwpPrior, grid: Sequence[float], rank: int, ranks: int,
+                      allgather, config: IeksConfig = IeksConfig(), want_cov=True, ctx=None) -> ShardReport:
+    """para_ieks over the time-axis shard `rank` of `ranks` (one process per
+    GPU).  `allgather(send: ndarray) -> ndarray` gathers every
+    rank's equally sized float64 vector in rank order (torch_allgather())."""
+    c = _ctx(ctx)
+    grid = _f64(grid)
+    n1 = grid.shape[0]
+    D, d = prior.state_dim, prior.dim
+    first, cnt = shard_range(n1, rank, ranks)
+    means = _result_array((cnt, D))
+    cov = _result_array((cnt, D, D)) if want_cov else None
+    sm = _result_array((cnt, d))
+    sc = _result_array((cnt, d, d)) if want_cov else None
+    trace = np.zeros(max(config.max_iterations, 1))
+    rep = A.IeksReport(_p(means), _p(cov), _p(sm), _p(sc), _p(trace), trace.shape[0], A.PODE_HOST,
+                       0, 0, 0.0, A.ScanStats())
+    comm, failure = make_shard_comm(rank, ranks, allgather)
+    pr = ivp._c()
+    prior_c = A.Prior(prior.nu, prior.dim, prior.sigma)
+    lin = {"ek1": 0, "ek0": 1}[config.linearization]
+    cfg = A.IeksConfig(config.max_iterations, config.traj_rtol, config.obj_atol, config.obj_rtol, lin)
+    st = A.Status()
+    rc = c._lib.pode_ieks_sharded(c.handle, C.byref(pr), C.byref(prior_c), _p(grid), n1, C.byref(cfg),
+                                  C.byref(comm), C.byref(rep), C.byref(st))
+    if failure:
+        raise failure[0]
+    _raise(rc, st)
+    return ShardReport(first, grid[first:first + cnt].copy(), means, cov, sm, sc, rep.sigma_hat, rep.iterations,
+                       trace[:rep.iterations].copy(), bool(rep.converged))

@@ -567,4 +567,65 @@ int pode_ieks(pode_context* ctx, const pode_problem* problem, const pode_prior* 
   });
 }
 
+void pode_shard_range(int64_t n_nodes, int32_t rank, int32_t ranks, int64_t* first_node, int64_t* count) {
+  const int64_t N = n_nodes - 1;
+  const int64_t lo = shard_first_step(N, rank, ranks), hi = shard_first_step(N, rank + 1, ranks);
+  if (first_node) *first_node = lo;
+  if (count) *count = (hi - lo) + (rank == ranks - 1 ? 1 : 0);
+}
+
+int pode_ieks_sharded(pode_context* ctx, const pode_problem* problem, const pode_prior* prior, const double* grid,
+                      int64_t n_nodes, const pode_ieks_config* config, const pode_shard_comm* comm,
+                      pode_ieks_report* report, pode_status* status) {
+  return guarded(status, [&] {
+    check_ctx(ctx);
+    if (problem == nullptr || prior == nullptr || grid == nullptr || config == nullptr || report == nullptr ||
+        comm == nullptr || comm->allgather == nullptr)
+      throw ApiError(PODE_ERR_INVALID_INPUT, "ieks_sharded: NULL argument");
+    if (comm->ranks < 1 || comm->rank < 0 || comm->rank >= comm->ranks)
+      throw ApiError(PODE_ERR_INVALID_INPUT, "ieks_sharded: rank outside [0, ranks)");
+    const host::Problem p = host::resolve_problem(*problem);
+    if (p.dim != prior->dim) throw ApiError(PODE_ERR_DIMENSION, "ieks: problem and prior dimensions disagree");
+    if (config->max_iterations < 1) throw ApiError(PODE_ERR_INVALID_INPUT, "ieks: max_iterations must be at least 1");
+    if (prior->nu < 1 || prior->dim < 1) throw ApiError(PODE_ERR_INVALID_INPUT, "IwpPrior: need nu >= 1 and dim >= 1");
+    if (!(prior->sigma >= 0.0) || !std::isfinite(prior->sigma))
+      throw ApiError(PODE_ERR_INVALID_INPUT, "IwpPrior: sigma must be finite and nonnegative");
+    if (n_nodes - 1 < comm->ranks) throw ApiError(PODE_ERR_INVALID_INPUT, "ieks_sharded: fewer steps than shards");
+    if (grid[0] != 0.0) throw ApiError(PODE_ERR_INVALID_INPUT, "discretize: grid must start at t = 0");
+    for (int64_t n = 0; n + 1 < n_nodes; ++n)
+      if (!(grid[n + 1] > grid[n])) throw ApiError(PODE_ERR_INVALID_INPUT, "discretize: grid must be strictly increasing");
+    const int D = prior->dim * (prior->nu + 1);
+    const auto& ops = ops_for(D);
+    if (ops.ieks_sharded == nullptr) throw ApiError(PODE_ERR_UNSUPPORTED, "ieks_sharded: state dimension not compiled");
+    int64_t first = 0, nloc = 0;
+    pode_shard_range(n_nodes, comm->rank, comm->ranks, &first, &nloc);
+    const bool dev = report->location == PODE_DEVICE;
+    const int d = prior->dim;
+    // the last shard's engine writes node N too; others write nloc nodes
+    double* means = dev ? report->means : (report->means ? ctx->ws.arr<double>("out_means", (nloc + 1) * D) : nullptr);
+    double* cov =
+        dev ? report->cov_sqrt : (report->cov_sqrt ? ctx->ws.arr<double>("out_cov", (nloc + 1) * D * D) : nullptr);
+    double* sm = dev ? report->solution_means
+                     : (report->solution_means ? ctx->ws.arr<double>("out_sm", (nloc + 1) * d) : nullptr);
+    double* sc = dev ? report->solution_covs
+                     : (report->solution_covs ? ctx->ws.arr<double>("out_sc", (nloc + 1) * d * d) : nullptr);
+    IeksResult r;
+    ops.ieks_sharded(ctx, p, *prior, grid, n_nodes, *config, *comm, means, cov, sm, sc, &r);
+    if (!dev) {
+      stage_out(ctx, report->means, means, size_t(nloc) * D, false);
+      stage_out(ctx, report->cov_sqrt, cov, size_t(nloc) * D * D, false);
+      stage_out(ctx, report->solution_means, sm, size_t(nloc) * d, false);
+      stage_out(ctx, report->solution_covs, sc, size_t(nloc) * d * d, false);
+    }
+    raise_device_error(ctx, "ieks: calibration");
+    report->iterations = r.iterations;
+    report->converged = r.converged ? 1 : 0;
+    report->sigma_hat = r.sigma_hat;
+    report->scan_stats = {r.stats.combines, r.stats.depth};
+    if (report->objective_trace)
+      for (int k = 0; k < int(r.trace.size()) && k < report->trace_capacity; ++k)
+        report->objective_trace[k] = r.trace[k];
+  });
+}
+
 }  // extern "C"

@@ -25,7 +25,14 @@ struct EngineOps {
   void (*rts)(pode_context*, const DevChain&, double*, double*, double*, double*, ScanTally*);
   void (*ieks)(pode_context*, const host::Problem&, const pode_prior&, const double*, int64_t,
                const pode_ieks_config&, double*, double*, double*, double*, IeksResult*);
+  // time-axis shard of the fused engine (nullptr where it is not compiled)
+  void (*ieks_sharded)(pode_context*, const host::Problem&, const pode_prior&, const double*, int64_t,
+                       const pode_ieks_config&, const pode_shard_comm&, double*, double*, double*, double*,
+                       IeksResult*);
 };
+
+// Shard s of R owns steps [floor(N s / R), floor(N (s+1) / R)).
+inline int64_t shard_first_step(int64_t N, int s, int R) { return (N * s) / R; }
 
 constexpr int kMinD = 1;
 constexpr int kMaxD = 16;

@@ -605,6 +605,35 @@ struct Engine {
     cudaFuncSetAttribute(k_scan_down<D, SOps<D>, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(k_scan_reduce<D, MOps<D>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(k_scan_down<D, MOps<D>, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_combine<D, MOps<D>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  }
+
+  // In-order total x[0] ⊗ .. ⊗ x[n-1] (fan-in-4 reduce tree, any Op); the
+  // result is element 0 of the returned array.
+  template <class Op>
+  static typename Op::Arr reduce_total(pode_context* ctx, typename Op::Arr x, int64_t n, const std::string& tag) {
+    set_smem();
+    DevError* err = reinterpret_cast<DevError*>(ctx->d_err);
+    int level = 0;
+    while (n > 1) {
+      const int L = 4;
+      const int64_t nb = (n + L - 1) / L;
+      typename Op::Arr agg = alloc<Op>(ctx, tag + std::to_string(level++), nb);
+      k_scan_reduce<D, Op><<<blocks_for<D>(nb), kThreads, smem_bytes<D>(), ctx->stream>>>(x, n, L, agg, err);
+      note_launch(ctx, Op::kReduce);
+      x = agg;
+      n = nb;
+    }
+    return x;
+  }
+
+  // out[0] = l[0] ⊗ r[0] (one element).
+  template <class Op>
+  static void combine_one(pode_context* ctx, typename Op::Arr l, typename Op::Arr r, typename Op::Arr o) {
+    set_smem();
+    k_combine<D, Op><<<1, kThreads, smem_bytes<D>(), ctx->stream>>>(1, l, r, o,
+                                                                    reinterpret_cast<DevError*>(ctx->d_err));
+    note_launch(ctx, "combine");
   }
 
   // Inclusive ⊗_f scan of a sequence whose first element is Gaussian

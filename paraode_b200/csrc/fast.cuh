@@ -48,6 +48,15 @@ struct FastArgs {
   double* pair0;
   double* pair1;
   int64_t term_off;
+  // Time-axis shard: local node 0 is global node g0 (grid
+  // points at the global grid + g0).  first: this shard starts at global
+  // node 0 (chunk 0 absorbs the initial distribution); otherwise chunk 0
+  // starts from `carry` = the filtered (b, C) at local node 0 folded from the
+  // preceding shards.  last: this shard ends at global node N (terminal
+  // element, node N counted in the stopping maxima and written out).
+  int first = 1;
+  int last = 1;
+  const double* carry = nullptr;  // D + D*D doubles
 };
 
 // The linearisation point of this iteration (graph-loop mode).

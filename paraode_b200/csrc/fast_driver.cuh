@@ -279,6 +279,264 @@ struct FastEngine {
     return res;
   }
 
+  // ------------------------------------------------ time-axis shards ---
+  static constexpr int kFel = 3 * D * D + 2 * D;  // one filtering element
+  static constexpr int kSel = 2 * D * D + D;      // one smoothing element
+  // element views of a contiguous per-element buffer
+  static FEd fview(double* b) {
+    FEd e;
+    e.a = b;
+    e.c = b + D * D;
+    e.j = b + 2 * D * D;
+    e.b = b + 3 * D * D;
+    e.eta = b + 3 * D * D + D;
+    return e;
+  }
+  static SEd sview(double* b) { return SEd{b, b + 2 * D * D, b + D * D}; }  // {e, g, l}
+  static void d2d(pode_context* ctx, double* dst, const double* src, size_t n) {
+    if (src == nullptr || dst == nullptr) return;
+    cuda_check(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream), "shard copy");
+  }
+  static void fel_move(pode_context* ctx, const FEd& src, int64_t i, const FEd& dst, int64_t j) {
+    d2d(ctx, dst.a + j * D * D, src.a + i * D * D, D * D);
+    d2d(ctx, dst.c + j * D * D, src.c + i * D * D, D * D);
+    d2d(ctx, dst.j + j * D * D, src.j + i * D * D, D * D);
+    d2d(ctx, dst.b + j * D, src.b + i * D, D);
+    d2d(ctx, dst.eta + j * D, src.eta + i * D, D);
+  }
+  static void sel_move(pode_context* ctx, const SEd& src, int64_t i, const SEd& dst, int64_t j, bool with_l) {
+    d2d(ctx, dst.e + j * D * D, src.e + i * D * D, D * D);
+    d2d(ctx, dst.g + j * D, src.g + i * D, D);
+    if (with_l) d2d(ctx, dst.l + j * D * D, src.l + i * D * D, D * D);
+  }
+
+  // All-gather of one contiguous device element (count doubles) from every
+  // shard; the R copies land contiguously in dev_all (rank order).
+  static void gather(pode_context* ctx, const pode_shard_comm& comm, const double* dev_own, int64_t count,
+                     double* dev_all, std::vector<double>* host_all = nullptr) {
+    std::vector<double> send(static_cast<size_t>(count)), recv(static_cast<size_t>(count) * comm.ranks);
+    cuda_check(cudaMemcpyAsync(send.data(), dev_own, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream),
+               "shard send");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "shard sync");
+    if (comm.allgather(comm.user, send.data(), count, recv.data()) != 0)
+      throw ApiError(PODE_ERR_INVALID_INPUT, "ieks_sharded: all-gather failed");
+    if (dev_all)
+      cuda_check(cudaMemcpyAsync(dev_all, recv.data(), sizeof(double) * recv.size(), cudaMemcpyHostToDevice,
+                                 ctx->stream),
+                 "shard recv");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "shard sync");
+    if (host_all) *host_all = std::move(recv);
+  }
+
+  // Fixed-order fold of the gathered scalars (sum, max, max) of every shard.
+  static void gather3(pode_context* ctx, const pode_shard_comm& comm, const double* dev3, double (&out)[3],
+                      bool& any_failed, bool own_failed) {
+    double* tmp = ctx->ws.arr<double>("sh_s3", 4);
+    cuda_check(cudaMemcpyAsync(tmp, dev3, sizeof(double) * 3, cudaMemcpyDeviceToDevice, ctx->stream), "s3");
+    const double flag = own_failed ? 1.0 : 0.0;
+    cuda_check(cudaMemcpyAsync(tmp + 3, &flag, sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "s3 flag");
+    std::vector<double> all;
+    gather(ctx, comm, tmp, 4, nullptr, &all);
+    out[0] = 0.0;
+    out[1] = 0.0;
+    out[2] = 0.0;
+    any_failed = false;
+    for (int r = 0; r < comm.ranks; ++r) {
+      out[0] += all[size_t(r) * 4 + 0];
+      out[1] = std::max(out[1], all[size_t(r) * 4 + 1]);
+      out[2] = std::max(out[2], all[size_t(r) * 4 + 2]);
+      any_failed |= all[size_t(r) * 4 + 3] != 0.0;
+    }
+  }
+
+  // para_ieks over the time-axis shard `comm.rank`: the same
+  // passes on the local steps, plus three exchanges per iteration (forward
+  // aggregate -> Gaussian carry, backward aggregate -> right mean carry,
+  // stopping scalars).  Per-iteration host loop (the exchanges are host
+  // collectives).
+  static IeksResult run_sharded(pode_context* ctx, const host::Problem& p, const pode_prior& prior,
+                                const double* grid_h, int64_t n1g, const pode_ieks_config& cfg,
+                                const pode_shard_comm& comm, double* means, double* cov, double* sol_m,
+                                double* sol_c) {
+    using IE = IeksEngine<D>;
+    const int R = comm.ranks, rank = comm.rank;
+    IeksSetup<D> s;
+    IE::setup(ctx, p, prior, grid_h, n1g, s);
+    cudaStream_t st = ctx->stream;
+    Workspace& ws = ctx->ws;
+    const int64_t Ng = s.N;
+    const int64_t g0 = shard_first_step(Ng, rank, R);
+    const int64_t N = shard_first_step(Ng, rank + 1, R) - g0;  // local steps
+    if (N < 1) throw ApiError(PODE_ERR_INVALID_INPUT, "ieks_sharded: fewer steps than shards");
+    const int L = chunk_len(ctx, N);
+    const int64_t nc = (N + L - 1) / L;
+    FastConst<D> cst;
+    std::memcpy(cst.q, s.h_q.data(), sizeof(cst.q));
+    std::memcpy(cst.qunit, s.h_qunit.data(), sizeof(cst.qunit));
+    std::memcpy(cst.qunit_rdiag, s.h_qinv.data(), sizeof(cst.qunit_rdiag));
+    std::memcpy(cst.m0, s.h_m0.data(), sizeof(cst.m0));
+    const size_t padded = size_t(nc) * L;
+    double* eta_a = ws.arr<double>("lane_eta_a", padded * D + D);
+    double* eta_b = ws.arr<double>("lane_eta_b", padded * D + D);
+    FEd agg = Engine<D>::template alloc<FOps<D>>(ctx, "fast_agg", nc);
+    lane::ElemSoA soa;
+    {
+      double* base = ws.arr<double>("fast_elems", padded * (D * D + D) + D);
+      soa = lane::ElemSoA{base, base + padded * D * D, base + padded * (D * D + D), nc, L};
+    }
+    SEd bagg = Engine<D>::template alloc<MOps<D>>(ctx, "sh_bagg", nc);
+    const unsigned lblocks = static_cast<unsigned>((nc + lane::kLaneThreads - 1) / lane::kLaneThreads);
+    const int64_t nparts = int64_t(lblocks);
+    double* part = ws.arr<double>("fast_part", nparts * 3 + 3);
+    double* red = part + nparts * 3;
+    const unsigned th = lane::kLaneThreads;
+    auto term = [&](double* base) { return base + padded * D; };
+    // exchange buffers: R gathered elements + own element + carry (b, C)
+    double* xf = ws.arr<double>("sh_xf", size_t(R + 2) * kFel);
+    double* xs = ws.arr<double>("sh_xs", size_t(R + 2) * kSel);
+    double* carry = ws.arr<double>("sh_carry", D + D * D);
+    FastArgs a{s.grid + g0, eta_a, term(eta_a), N, L, nc, cfg.linearization, s.prob,
+               reinterpret_cast<DevError*>(ctx->d_err)};
+    a.first = rank == 0 ? 1 : 0;
+    a.last = rank == R - 1 ? 1 : 0;
+    a.carry = carry;
+
+    // forward exchange: agg[0] <- (t_0 ⊗ .. ⊗ t_{rank-1}) ⊗ agg[0]; carry = its (b, C)
+    auto forward_exchange = [&]() {
+      const FEd tot = Engine<D>::template reduce_total<FOps<D>>(ctx, agg, nc, "sh_fred_");
+      double* own = xf + size_t(R) * kFel;
+      fel_move(ctx, tot, 0, fview(own), 0);
+      gather(ctx, comm, own, kFel, xf);
+      if (rank == 0) return;
+      for (int i = 1; i < rank; ++i)
+        Engine<D>::template combine_one<FOps<D>>(ctx, fview(xf), fview(xf + size_t(i) * kFel), fview(xf));
+      d2d(ctx, carry, fview(xf).b, D);
+      d2d(ctx, carry + D, fview(xf).c, D * D);
+      double* tmp = xf + size_t(R + 1) * kFel;
+      fel_move(ctx, agg, 0, fview(tmp), 0);
+      Engine<D>::template combine_one<FOps<D>>(ctx, fview(xf), fview(tmp), fview(tmp));
+      fel_move(ctx, fview(tmp), 0, agg, 0);
+    };
+    // backward exchange: bagg[nc-1] <- bagg[nc-1] ⊗ (t_{rank+1} ⊗ .. ⊗ t_{R-1});
+    // the incoming smoothed mean at the halo node -> elems.term
+    auto backward_exchange = [&]() {
+      const SEd tot = Engine<D>::template reduce_total<MOps<D>>(ctx, bagg, nc, "sh_bred_");
+      double* own = xs + size_t(R) * kSel;
+      sel_move(ctx, tot, 0, sview(own), 0, false);
+      gather(ctx, comm, own, kSel, xs);
+      if (rank == R - 1) return;
+      double* acc = xs + size_t(R - 1) * kSel;
+      for (int i = R - 2; i > rank; --i)
+        Engine<D>::template combine_one<MOps<D>>(ctx, sview(xs + size_t(i) * kSel), sview(acc), sview(acc));
+      double* tmp = xs + size_t(R + 1) * kSel;
+      sel_move(ctx, bagg, nc - 1, sview(tmp), 0, false);
+      Engine<D>::template combine_one<MOps<D>>(ctx, sview(tmp), sview(acc), sview(tmp));
+      sel_move(ctx, sview(tmp), 0, bagg, nc - 1, false);
+      d2d(ctx, soa.term, sview(acc).g, D);
+    };
+
+    lane::k_eta_fill<D><<<grid1(int64_t(padded) * D + D), kRedThreads, 0, st>>>(s.mu0, nc, L, eta_a);
+    note_launch(ctx, "fill");
+    reset_error(ctx);
+    // objective of the constant start (ieks.cpp:147-148)
+    lane::k_lane_bwd_down<D, d, true><<<lblocks, th, 0, st>>>(a, cst, soa, bagg, eta_a, term(eta_a), eta_b,
+                                                               term(eta_b), part);
+    note_launch(ctx, "fast_objective");
+    k_finish3<<<1, kRedThreads, 0, st>>>(part, nparts, red);
+    note_launch(ctx, "finish3");
+    double r3[3];
+    bool any_failed = false;
+    gather3(ctx, comm, red, r3, any_failed, false);
+    double v_prev = 0.5 * r3[0];
+
+    IeksResult res;
+    int it = 0;
+    while (it < cfg.max_iterations) {
+      ++it;
+      reset_error(ctx);
+      a.eta = eta_a;
+      a.eta_term = term(eta_a);
+      lane::k_lane_fwd_reduce<D, d><<<lblocks, th, 0, st>>>(a, cst, agg);
+      note_launch(ctx, "fast_fwd_reduce");
+      forward_exchange();
+      const ScanTally tf = Engine<D>::scan_filtering_gauss(ctx, nc, agg, agg, scan_fanin());
+      lane::k_lane_fwd_down<D, d><<<lblocks, th, 0, st>>>(a, cst, agg, soa);
+      note_launch(ctx, "fast_fwd_down");
+      lane::k_lane_bfold<D><<<lblocks, th, 0, st>>>(soa, N, L, nc, bagg, a.last);
+      note_launch(ctx, "fast_bwd_fold");
+      backward_exchange();
+      const ScanTally tr = Engine<D>::scan_means_terminal(ctx, nc, bagg, scan_fanin());
+      lane::k_lane_bwd_down<D, d, false><<<lblocks, th, 0, st>>>(a, cst, soa, bagg, eta_a, term(eta_a), eta_b,
+                                                                  term(eta_b), part);
+      note_launch(ctx, "fast_bwd_down");
+      k_finish3<<<1, kRedThreads, 0, st>>>(part, nparts, red);
+      note_launch(ctx, "finish3");
+      const unsigned long long key = fetch_error(ctx);
+      gather3(ctx, comm, red, r3, any_failed, key != ~0ull);
+      if (key != ~0ull) IE::check_linearization(ctx, s, it);  // throws this shard's error
+      if (any_failed) throw ApiError(PODE_ERR_SINGULAR_FACTOR, "ieks_sharded: another shard failed", 0, 0.0, it);
+      res.stats.combines = std::max(res.stats.combines, (Ng - nc * R) + tf.combines * R + Ng);
+      res.stats.depth = std::max(res.stats.depth, int64_t(L) + tf.depth + int64_t(L) + tr.depth + 2 * R);
+      const double v = 0.5 * r3[0];
+      res.trace.push_back(v);
+      const bool conv = (r3[1] <= cfg.traj_rtol * r3[2]) ||
+                        (std::fabs(v - v_prev) <= cfg.obj_atol + cfg.obj_rtol * std::fabs(v));
+      std::swap(eta_a, eta_b);
+      v_prev = v;
+      if (conv) {
+        res.converged = true;
+        break;
+      }
+    }
+    res.iterations = it;
+
+    // finalize on the shard (eta_a: newest trajectory, eta_b: linearisation point)
+    a.eta = eta_b;
+    a.eta_term = term(eta_b);
+    double* cf = ws.arr<double>("fin_cf", padded * D * D + D * D);
+    double* cterm = cf + padded * D * D;
+    reset_error(ctx);
+    lane::k_lane_fwd_down<D, d, true><<<lblocks, th, 0, st>>>(a, cst, agg, soa, cf, cterm, part);
+    note_launch(ctx, "fin_fwd");
+    k_finish3<<<1, kRedThreads, 0, st>>>(part, lblocks, red);
+    note_launch(ctx, "finish3");
+    {
+      const unsigned long long key = fetch_error(ctx);
+      gather3(ctx, comm, red, r3, any_failed, key != ~0ull);
+      if (key != ~0ull) IE::check_linearization(ctx, s, it);
+      if (any_failed) throw ApiError(PODE_ERR_SINGULAR_FACTOR, "ieks_sharded: another shard failed", 0, 0.0, it);
+    }
+    const double innov = r3[0];
+    cuda_check(cudaMemcpyAsync(red, &innov, sizeof(double), cudaMemcpyHostToDevice, st), "innov");
+    SEd sagg = Engine<D>::template alloc<SOps<D>>(ctx, "fin_sagg", nc);
+    lane::k_lane_fin_fold<D, d><<<lblocks, th, 0, st>>>(a, cst, soa, cf, cterm, sagg);
+    note_launch(ctx, "fin_fold");
+    {  // right carry of the full smoothing aggregates: (E = 0, g, L) at the halo node
+      const SEd tot = Engine<D>::template reduce_total<SOps<D>>(ctx, sagg, nc, "sh_sred_");
+      double* own = xs + size_t(R) * kSel;
+      sel_move(ctx, tot, 0, sview(own), 0, true);
+      gather(ctx, comm, own, kSel, xs);
+      if (rank < R - 1) {
+        double* acc = xs + size_t(R - 1) * kSel;
+        for (int i = R - 2; i > rank; --i)
+          Engine<D>::template combine_one<SOps<D>>(ctx, sview(xs + size_t(i) * kSel), sview(acc), sview(acc));
+        double* tmp = xs + size_t(R + 1) * kSel;
+        sel_move(ctx, sagg, nc - 1, sview(tmp), 0, true);
+        Engine<D>::template combine_one<SOps<D>>(ctx, sview(tmp), sview(acc), sview(tmp));
+        sel_move(ctx, sview(tmp), 0, sagg, nc - 1, true);
+        d2d(ctx, cterm, sview(acc).l, D * D);
+      }
+    }
+    Engine<D>::scan_smoothing(ctx, nc, sagg, sagg, true);
+    const double count = double(Ng) * s.dim;
+    lane::k_lane_fin_bwd<D, d><<<lblocks, th, 0, st>>>(a, cst, soa, cf, cterm, sagg, eta_a, term(eta_a), red, count,
+                                                       lane::FinOut{means, cov, sol_m, sol_c});
+    note_launch(ctx, "fin_bwd");
+    IE::check_linearization(ctx, s, it);  // syncs
+    res.sigma_hat = std::sqrt(innov / count) * prior.sigma;
+    return res;
+  }
+
   // Lane finalize at the final linearisation point (the last iteration's
   // pass-B prefixes in `agg` are still valid for it): F1 filter + C_f(k) +
   // innovations, F2 chunk smoothing aggregates (E, g, L), a reverse ⊗_s scan

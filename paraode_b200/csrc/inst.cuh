@@ -74,7 +74,35 @@ void ik(pode_context* c, const host::Problem& p, const pode_prior& pr, const dou
   }
   *out = IeksEngine<kD>::run(c, p, pr, g, n1, cfg, m, cv, sm, sc);
 }
-const EngineOps kOps{kD, cf, cs, mf, ms, sf, ss, rt, ik};
+// Time-axis shard: the fused engine only.
+void iks(pode_context* c, const host::Problem& p, const pode_prior& pr, const double* g, int64_t n1,
+         const pode_ieks_config& cfg, const pode_shard_comm& comm, double* m, double* cv, double* sm, double* sc,
+         IeksResult* out) {
+  switch (pr.dim) {
+    case 1:
+      if constexpr (kFastOk<kD, 1>) {
+        *out = FastEngine<kD, 1>::run_sharded(c, p, pr, g, n1, cfg, comm, m, cv, sm, sc);
+        return;
+      }
+      break;
+    case 2:
+      if constexpr (kFastOk<kD, 2>) {
+        *out = FastEngine<kD, 2>::run_sharded(c, p, pr, g, n1, cfg, comm, m, cv, sm, sc);
+        return;
+      }
+      break;
+    case 3:
+      if constexpr (kFastOk<kD, 3>) {
+        *out = FastEngine<kD, 3>::run_sharded(c, p, pr, g, n1, cfg, comm, m, cv, sm, sc);
+        return;
+      }
+      break;
+    default:
+      break;
+  }
+  throw ApiError(PODE_ERR_UNSUPPORTED, "ieks_sharded: needs an ODE operator the fused engine serves (d <= 3, D <= 9)");
+}
+const EngineOps kOps{kD, cf, cs, mf, ms, sf, ss, rt, ik, iks};
 }  // namespace
 
 const EngineOps* PODE_CAT(engine_ops_d, PODE_D)() { return &kOps; }

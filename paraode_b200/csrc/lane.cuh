@@ -292,8 +292,9 @@ struct Model {
       for (int j = 0; j < D; ++j) cm[r][j] = (j <= r) ? m[r][j] : 0.0;
   }
 
-  __device__ static void taus(const double* grid, int64_t n, double (&t)[B], double (&ti)[B]) {
-    const double h = (n == 0) ? grid[1] - grid[0] : grid[n] - grid[n - 1];
+  // origin: local node 0 is global node 0 (its scale uses the first step).
+  __device__ static void taus(const double* grid, int origin, int64_t n, double (&t)[B], double (&ti)[B]) {
+    const double h = (n == 0 && origin) ? grid[1] - grid[0] : grid[n] - grid[n - 1];
     const double rh = sqrt(h);
     double fact = 1.0;
 #pragma unroll
@@ -427,20 +428,20 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(FastArgs a, Fa
   for (int r = 0; r < D; ++r) {
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      A[r][j] = (c != 0 && r == j) ? 1.0 : 0.0;
+      A[r][j] = (!(c == 0 && a.first) && r == j) ? 1.0 : 0.0;
       C[r][j] = 0.0;
       J[r][j] = 0.0;
     }
-    b[r] = (c == 0) ? cst.m0[r] : 0.0;
+    b[r] = (c == 0 && a.first) ? cst.m0[r] : 0.0;
     eta[r] = 0.0;
   }
   double tk[B], tki[B];
-  M::taus(a.grid, s, tk, tki);
+  M::taus(a.grid, a.first, s, tk, tki);
   bool bad_sing = false;
   int64_t bad_lin = -1;
   for (int64_t k = s; k < e; ++k) {
     double tn[B], tni[B], ratio[B], pc[B][B];
-    M::taus(a.grid, k + 1, tn, tni);
+    M::taus(a.grid, a.first, k + 1, tn, tni);
 #pragma unroll
     for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
     M::phi_coefs(ratio, pc);
@@ -552,25 +553,29 @@ __device__ __forceinline__ double fwd_down_chunk(FastArgs a, const FastConst<D>&
   const int64_t s = c * a.L;
   const int64_t e = min(a.N, s + a.L);
   double m[D], C[D][D];
-  if (c == 0) {
+  if (c == 0 && a.first) {
 #pragma unroll
     for (int r = 0; r < D; ++r) {
       m[r] = cst.m0[r];
 #pragma unroll
       for (int j = 0; j < D; ++j) C[r][j] = 0.0;
     }
+  } else if (c == 0) {  // shard > 0: the filtered marginal folded from the left
+    ld_mat<D>(a.carry + D, C);
+#pragma unroll
+    for (int r = 0; r < D; ++r) m[r] = a.carry[r];
   } else {
     ld_mat<D>(prefix.c + (c - 1) * D * D, C);
 #pragma unroll
     for (int r = 0; r < D; ++r) m[r] = prefix.b[(c - 1) * D + r];
   }
   double tk[B], tki[B];
-  M::taus(a.grid, s, tk, tki);
+  M::taus(a.grid, a.first, s, tk, tki);
   bool bad_sing = false;
   int64_t bad_lin = -1;
   for (int64_t k = s; k < e; ++k) {
     double tn[B], tni[B], ratio[B], pc[B][B];
-    M::taus(a.grid, k + 1, tn, tni);
+    M::taus(a.grid, a.first, k + 1, tn, tni);
 #pragma unroll
     for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
     M::phi_coefs(ratio, pc);
@@ -689,12 +694,12 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
 // terminal node N, so its aggregate has E = 0.
 template <int D>
 __global__ void __launch_bounds__(kLaneThreads) k_lane_bfold(ElemSoA elems, int64_t N, int L, int64_t nchunks,
-                                                             SEd bagg) {
+                                                             SEd bagg, int terminal = 1) {
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (c >= nchunks) return;
   const int64_t s = c * L;
   const int64_t e = min(N, s + L);
-  const bool last = c == nchunks - 1;
+  const bool last = c == nchunks - 1 && terminal;
   double Eg[D][D], gg[D];
   soa_ld<D>(elems, c, 0, Eg, gg);
   for (int64_t k = s + 1; k <= e; ++k) {
@@ -801,7 +806,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fin_fold(FastArgs a, Fast
   if (c >= a.nchunks) return;
   const int64_t s = c * a.L;
   const int64_t e = min(a.N, s + a.L);
-  const bool last = c == a.nchunks - 1;
+  const bool last = c == a.nchunks - 1 && a.last;
   double ea[D][D], la[D][D], ga[D];
 #pragma unroll
   for (int r = 0; r < D; ++r) {
@@ -813,10 +818,10 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fin_fold(FastArgs a, Fast
     }
   }
   double tn[B], tni[B];
-  M::taus(a.grid, e, tn, tni);
+  M::taus(a.grid, a.first, e, tn, tni);
   for (int64_t k = e - 1; k >= s; --k) {
     double tk[B], tki[B], ratio[B], pc[B][B];
-    M::taus(a.grid, k, tk, tki);
+    M::taus(a.grid, a.first, k, tk, tki);
 #pragma unroll
     for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
     M::phi_coefs(ratio, pc);
@@ -912,13 +917,13 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fin_bwd(FastArgs a, FastC
   if (c >= a.nchunks) return;
   const int64_t s = c * a.L;
   const int64_t e = min(a.N, s + a.L);
-  const bool last = c == a.nchunks - 1;
+  const bool last = c == a.nchunks - 1;  // cterm: C_f(N), or the right carry's factor (shards)
   const double sig = sqrt(innov[0] / count);
   double ls[D][D];
   ld_mat<D>(last ? cterm : suffix.l + (c + 1) * D * D, ls);
   double tn[B], tni[B];
-  M::taus(a.grid, e, tn, tni);
-  if (last) {
+  M::taus(a.grid, a.first, e, tn, tni);
+  if (last && a.last) {
     double eta[D];
 #pragma unroll
     for (int r = 0; r < D; ++r) eta[r] = eta_out_term[r];
@@ -926,7 +931,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fin_bwd(FastArgs a, FastC
   }
   for (int64_t k = e - 1; k >= s; --k) {
     double tk[B], tki[B], ratio[B], pc[B][B];
-    M::taus(a.grid, k, tk, tki);
+    M::taus(a.grid, a.first, k, tk, tki);
 #pragma unroll
     for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
     M::phi_coefs(ratio, pc);
@@ -978,7 +983,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, Fast
     const int64_t e = min(a.N, s + a.L);
     const bool last = c == a.nchunks - 1;
     double mu[D], te[B], tei[B];
-    M::taus(a.grid, e, te, tei);
+    M::taus(a.grid, a.first, e, te, tei);
     double bar_next[D];
 #pragma unroll
     for (int r = 0; r < D; ++r) {
@@ -992,9 +997,11 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, Fast
         eta_e = te[r % B] * mu[r];
       }
       if (last) {
-        if (!kInitial) new_term[r] = eta_e;
-        dmax = fmax(dmax, fabs(eta_e - old_e));
-        emax = fmax(emax, fabs(eta_e));
+        if (!kInitial) new_term[r] = eta_e;  // shards: the halo node, owned by the next shard
+        if (a.last) {
+          dmax = fmax(dmax, fabs(eta_e - old_e));
+          emax = fmax(emax, fabs(eta_e));
+        }
       }
       bar_next[r] = tei[r % B] * eta_e;
     }
@@ -1023,7 +1030,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, Fast
         for (int r = 0; r < D; ++r) on[r] = eta_old[((k - 1 - s) * D + r) * nc + c];
       }
       double tk[B], tki[B];
-      M::taus(a.grid, k, tk, tki);
+      M::taus(a.grid, a.first, k, tk, tki);
       double etak[D];
       if (kInitial) {
 #pragma unroll
