@@ -237,6 +237,7 @@ def run_reference(args):
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())  # functional runs: N ranks may share one GPU
     if world > 1:
         import torch.distributed as dist
         backend = os.environ.get("PODE_BENCH_BACKEND", "nccl")  # gloo: functional runs of N ranks on one GPU
