@@ -225,6 +225,12 @@ int pode_ieks(pode_context* ctx, const pode_problem* problem, const pode_prior* 
               const double* grid, int64_t n_nodes, const pode_ieks_config* config,
               pode_ieks_report* report, pode_status* status);
 
+/* Accuracy reference of the benchmark harness (problems.cpp:11-27): `steps`
+ * classical RK4 steps of the registered field on [0, t_end]; table holds
+ * (steps+1) * dim host doubles.  PODE_ERR_INVALID_INPUT if it diverges. */
+int pode_rk4_table(pode_context* ctx, const pode_problem* problem, int64_t steps, double* table,
+                   pode_status* status);
+
 /* ---- time-axis sharding (one process per GPU) ----------
  * The reference has no multi-device path; this is the SURVEY.md §8(e)
  * partition of the same solve.  Shard r of R owns steps [s_r, e_r),

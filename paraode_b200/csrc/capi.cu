@@ -13,6 +13,7 @@
 #include "dispatch.hpp"
 #include "engine.cuh"
 #include "host_model.hpp"
+#include "field.cuh"
 #include "ieks.cuh"
 
 namespace pode {
@@ -135,6 +136,35 @@ T* stage_in(pode_context* ctx, const std::string& tag, const T* src, size_t coun
 // caller's first-touch page faults are taken in parallel, not by the DMA
 // engine's pageable path).
 constexpr size_t kStageBytes = size_t(32) << 20;
+
+// Classical RK4 on a uniform grid by one thread (the accuracy reference of
+// the benchmark harness, problems.cpp:11-27; autonomous registered fields).
+constexpr int kRk4MaxDim = 28;
+
+template <int DMAX>
+__global__ void k_rk4(DevProblem prob, double t_end, int64_t steps, const double* y0, double* table, int* bad) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int d = prob.dim;
+  double y[DMAX], k1[DMAX], k2[DMAX], k3[DMAX], k4[DMAX], tmp[DMAX], jac[DMAX * DMAX];
+  for (int i = 0; i < d; ++i) table[i] = y[i] = y0[i];
+  const double h = t_end / double(steps);
+  bool finite = true;
+  for (int64_t n = 0; n < steps; ++n) {
+    eval_field<DMAX>(prob, y, k1, jac);
+    for (int i = 0; i < d; ++i) tmp[i] = y[i] + (0.5 * h) * k1[i];
+    eval_field<DMAX>(prob, tmp, k2, jac);
+    for (int i = 0; i < d; ++i) tmp[i] = y[i] + (0.5 * h) * k2[i];
+    eval_field<DMAX>(prob, tmp, k3, jac);
+    for (int i = 0; i < d; ++i) tmp[i] = y[i] + h * k3[i];
+    eval_field<DMAX>(prob, tmp, k4, jac);
+    for (int i = 0; i < d; ++i) {
+      y[i] += (h / 6.0) * (((k1[i] + 2.0 * k2[i]) + 2.0 * k3[i]) + k4[i]);
+      finite &= isfinite(y[i]);
+      table[(n + 1) * d + i] = y[i];
+    }
+  }
+  if (!finite) *bad = 1;
+}
 
 void copy_out_staged(pode_context* ctx, char* dst, const char* dev, size_t bytes) {
   cudaStream_t st = ctx->stream;
@@ -564,6 +594,35 @@ int pode_ieks(pode_context* ctx, const pode_problem* problem, const pode_prior* 
     if (report->objective_trace)
       for (int k = 0; k < int(r.trace.size()) && k < report->trace_capacity; ++k)
         report->objective_trace[k] = r.trace[k];
+  });
+}
+
+int pode_rk4_table(pode_context* ctx, const pode_problem* problem, int64_t steps, double* table,
+                   pode_status* status) {
+  return guarded(status, [&] {
+    check_ctx(ctx);
+    if (problem == nullptr || table == nullptr) throw ApiError(PODE_ERR_INVALID_INPUT, "rk4_reference: NULL argument");
+    if (steps < 1 || !(problem->t_end > 0.0))
+      throw ApiError(PODE_ERR_INVALID_INPUT, "rk4_reference: need positive step and horizon");
+    const host::Problem p = host::resolve_problem(*problem);
+    if (p.dim > kRk4MaxDim) throw ApiError(PODE_ERR_UNSUPPORTED, "rk4_reference: dimension too large");
+    DevProblem dp{};
+    dp.kind = p.kind;
+    dp.dim = p.dim;
+    for (size_t k = 0; k < p.params.size() && k < size_t(kMaxParams); ++k) dp.params[k] = p.params[k];
+    const size_t n = size_t(steps + 1) * p.dim;
+    double* y0 = ctx->ws.arr<double>("rk4_y0", p.dim);
+    double* dev = ctx->ws.arr<double>("rk4_table", n);
+    int* bad = ctx->ws.arr<int>("rk4_bad", 1);
+    cuda_check(cudaMemcpyAsync(y0, p.y0.data(), sizeof(double) * p.dim, cudaMemcpyHostToDevice, ctx->stream), "y0");
+    cuda_check(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream), "rk4 flag");
+    k_rk4<kRk4MaxDim><<<1, 32, 0, ctx->stream>>>(dp, p.t_end, steps, y0, dev, bad);
+    note_launch(ctx, "rk4");
+    int hbad = 0;
+    cuda_check(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "rk4 flag");
+    stage_out(ctx, table, dev, n, false);
+    cuda_check(cudaStreamSynchronize(ctx->stream), "rk4 sync");
+    if (hbad) throw ApiError(PODE_ERR_INVALID_INPUT, "rk4_reference: integration diverged");
   });
 }
 

@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kBWarps * 32, kGroupMinBlocks / 2) k_bscan_loc
 // sequential fan-in (throughput-bound).  PODE_BSCAN=0 disables, =n sets it.
 inline int64_t bscan_max() {
   const char* env = std::getenv("PODE_BSCAN");
-  if (env == nullptr) return 4096;
+  if (env == nullptr || *env == '\0') return 4096;
   const long long v = std::atoll(env);
   return v == 1 ? (int64_t(1) << 62) : int64_t(v);
 }

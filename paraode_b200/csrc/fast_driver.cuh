@@ -74,7 +74,7 @@ struct FastEngine {
   // host round trip per iteration) unless profiling or PODE_GRAPH=0.
   static bool use_graph(pode_context* ctx, const pode_ieks_config& cfg) {
     const char* env = std::getenv("PODE_GRAPH");
-    return !ctx->prof_on && cfg.max_iterations > 1 && !(env != nullptr && std::atoi(env) == 0);
+    return !ctx->prof_on && cfg.max_iterations > 1 && !(env != nullptr && *env != '\0' && std::atoi(env) == 0);
   }
 
   template <class Body>
@@ -127,14 +127,14 @@ struct FastEngine {
   // ⊗_f needs ~250 live doubles per thread and spills.
   static int scan_fanin() {
     const char* env = std::getenv("PODE_SCAN_FANIN");
-    const int v = env ? std::atoi(env) : 4;
+    const int v = (env && *env) ? std::atoi(env) : 4;
     return v >= 2 ? v : 4;
   }
 
   // One chunk per thread, ~256 resident threads per SM.
   static int chunk_len(pode_context* ctx, int64_t N) {
-    const char* env = std::getenv("PODE_CHUNK");
-    if (env) return std::max(2, std::atoi(env));
+    const char* env = std::getenv("PODE_CHUNK");  // unset or empty: the default below
+    if (env && *env) return std::max(2, std::atoi(env));
     const int64_t target = int64_t(ctx->sm_count) * 256;
     const int64_t L = (N + target - 1) / target;
     return static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(L, 4096)));

@@ -25,6 +25,12 @@ namespace pode {
 namespace lane {
 
 constexpr int kLaneThreads = 128;
+// The streaming backward passes (C2, E) are HBM-bound: more resident warps
+// keep more loads in flight (register cap 64K / (128 * kBwdMinBlocks)).
+#ifndef PODE_BWD_MIN_BLOCKS
+#define PODE_BWD_MIN_BLOCKS 2
+#endif
+constexpr int kBwdMinBlocks = PODE_BWD_MIN_BLOCKS;
 
 // Householder LQ of an R x K row-major register matrix over the first P
 // pivots: row p is reflected against columns p..K-1 and every later row is
@@ -693,7 +699,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, Fast
 // (⊗_s on means, parallel.cpp:146-156); the last chunk includes the
 // terminal node N, so its aggregate has E = 0.
 template <int D>
-__global__ void __launch_bounds__(kLaneThreads) k_lane_bfold(ElemSoA elems, int64_t N, int L, int64_t nchunks,
+__global__ void __launch_bounds__(kLaneThreads, kBwdMinBlocks) k_lane_bfold(ElemSoA elems, int64_t N, int L, int64_t nchunks,
                                                              SEd bagg, int terminal = 1) {
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (c >= nchunks) return;
@@ -960,7 +966,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fin_bwd(FastArgs a, FastC
 // layout of eta_at; the next step's (E, g, eta_old) are prefetched while the
 // current step computes.
 template <int D, int d, bool kInitial>
-__global__ void __launch_bounds__(kLaneThreads) k_lane_bwd_down(FastArgs a, FastConst<D> cst, ElemSoA elems,
+__global__ void __launch_bounds__(kLaneThreads, kBwdMinBlocks) k_lane_bwd_down(FastArgs a, FastConst<D> cst, ElemSoA elems,
                                                                 SEd suffix, const double* eta_old,
                                                                 const double* old_term, double* eta_new,
                                                                 double* new_term, double* part) {
