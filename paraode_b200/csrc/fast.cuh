@@ -59,13 +59,19 @@ struct FastArgs {
   const double* carry = nullptr;  // D + D*D doubles
 };
 
-// The linearisation point of this iteration (graph-loop mode).
-__device__ __forceinline__ void resolve_lin(FastArgs& a) {
-  if (a.it_dev != nullptr) {
+// The linearisation point of this iteration (its node-N slot in `term`).
+// Kernels keep their FastArgs parameter unmodified, so it stays in the
+// constant parameter bank (a written copy would be spilled to the stack).
+struct LinPoint {
+  const double* eta;
+  const double* term;
+};
+__device__ __forceinline__ LinPoint lin_point(const FastArgs& a) {
+  if (a.it_dev != nullptr) {  // graph-loop mode
     const double* b = (*a.it_dev & 1) ? a.pair1 : a.pair0;
-    a.eta = b;
-    a.eta_term = b + a.term_off;
+    return LinPoint{b, b + a.term_off};
   }
+  return LinPoint{a.eta, a.eta_term};
 }
 
 __device__ __forceinline__ double ipow(double h, int k) {

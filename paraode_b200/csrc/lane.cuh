@@ -340,12 +340,17 @@ __device__ __forceinline__ double eta_at(const double* base, const double* term,
   return (k == N) ? term[r] : base[eta_index<D>(k, r, L, nc)];
 }
 
-// y = E_0 eta_k (the solution components of node k).
+// y = E_0 eta at node k = s + t of chunk c (t = L: the next chunk's first
+// node; k = N: the node-N slot), without an integer division.
 template <int D, int d>
-__device__ __forceinline__ void gather_y(const FastArgs& a, int64_t k, double (&y)[d]) {
+__device__ __forceinline__ void gather_y(const FastArgs& a, const LinPoint& lp, int64_t c, int64_t t, int64_t k,
+                                         double (&y)[d]) {
   constexpr int B = D / d;
+  const bool at_n = k == a.N;
+  const bool wrap = t == a.L;
+  const int64_t cc = wrap ? c + 1 : c, tt = wrap ? 0 : t;
 #pragma unroll
-  for (int j = 0; j < d; ++j) y[j] = eta_at<D>(a.eta, a.eta_term, k, j * B, a.N, a.L, a.nchunks);
+  for (int j = 0; j < d; ++j) y[j] = at_n ? lp.term[j * B] : lp.eta[(tt * D + j * B) * a.nchunks + cc];
 }
 
 template <int D>
@@ -421,12 +426,12 @@ __device__ __forceinline__ void block_sum_partial(double* red, double v, double*
 // One thread per chunk: fold the chunk's filtering elements into the
 // aggregate (A, b, C, eta, J) (see fast.cuh for the algebra).
 template <int D, int d>
-__global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(FastArgs a, FastConst<D> cst, FEd agg) {
+__global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(const FastArgs a, FastConst<D> cst, FEd agg) {
   using M = Model<D, d>;
   constexpr int B = M::B;
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (c >= a.nchunks) return;
-  resolve_lin(a);
+  const LinPoint lp = lin_point(a);
   const int64_t s = c * a.L;
   const int64_t e = min(a.N, s + a.L);
   double A[D][D], C[D][D], J[D][D], b[D], eta[D];
@@ -458,7 +463,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(FastArgs a, Fa
     M::predict_cov(pc, C, cst.q, cm);
     // update at node k+1
     double ylin[d];
-    gather_y<D, d>(a, k + 1, ylin);
+    gather_y<D, d>(a, lp, c, k + 1 - s, k + 1, ylin);
     const typename M::Lin lin = M::linearize(a.prob, ylin, a.ek0);
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
     const typename M::Upd u = M::update(lin, tn, cm);
@@ -550,12 +555,12 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(FastArgs a, Fa
 // the whitened innovations ||S^-1 (H m- - offset)||^2 (innovation_stats,
 // ieks.cpp:79-104) into one partial per block.
 template <int D, int d, bool kFinal>
-__device__ __forceinline__ double fwd_down_chunk(FastArgs a, const FastConst<D>& cst, const FEd& prefix,
+__device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastConst<D>& cst, const FEd& prefix,
                                                  const ElemSoA& elems, double* cf, double* cterm, int64_t c) {
   using M = Model<D, d>;
   constexpr int B = M::B;
   double innov = 0.0;
-  resolve_lin(a);
+  const LinPoint lp = lin_point(a);
   const int64_t s = c * a.L;
   const int64_t e = min(a.N, s + a.L);
   double m[D], C[D][D];
@@ -643,7 +648,7 @@ __device__ __forceinline__ double fwd_down_chunk(FastArgs a, const FastConst<D>&
     soa_st<D>(elems, c, k - s, E, gk);
     // measurement update at node k+1
     double ylin[d];
-    gather_y<D, d>(a, k + 1, ylin);
+    gather_y<D, d>(a, lp, c, k + 1 - s, k + 1, ylin);
     const typename M::Lin lin = M::linearize(a.prob, ylin, a.ek0);
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
     const typename M::Upd u = M::update(lin, tn, cm);
@@ -684,7 +689,7 @@ __device__ __forceinline__ double fwd_down_chunk(FastArgs a, const FastConst<D>&
 }
 
 template <int D, int d, bool kFinal = false>
-__global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(FastArgs a, FastConst<D> cst, FEd prefix,
+__global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(const FastArgs a, FastConst<D> cst, FEd prefix,
                                                                 ElemSoA elems, double* cf = nullptr,
                                                                 double* cterm = nullptr, double* part = nullptr) {
   __shared__ double red[kFinal ? kLaneThreads : 1];
