@@ -262,5 +262,52 @@ SolverReport<Matrix, Vector> para_ieks(const Problem& problem, const IwpPrior& p
   return out;
 }
 
+// para_ieks over time-axis shard `rank` of `ranks` (one process per GPU;
+// DESIGN.md §6).  `allgather(send, count, recv)` gathers `count` doubles of
+// every rank into recv[rank * count + i] (MPI_Allgather, NCCL, ...) and
+// returns 0 on success.  The report holds this shard's nodes (times,
+// marginals, solution moments from pode_shard_range's first node on); the
+// scalars are those of the whole solve.
+template <class Matrix, class Vector>
+SolverReport<Matrix, Vector> para_ieks_sharded(const Problem& problem, const IwpPrior& prior,
+                                               const std::vector<double>& grid, const IeksConfig& config,
+                                               int rank, int ranks, pode_allgather_fn allgather, void* user,
+                                               Device& dev) {
+  const int D = prior.state_dim(), d = prior.dim;
+  const int64_t n1 = int64_t(grid.size());
+  int64_t first = 0, cnt = 0;
+  pode_shard_range(n1, rank, ranks, &first, &cnt);
+  pode_problem p{int32_t(problem.kind), problem.dim, problem.t_end, problem.y0.data(),
+                 problem.params.empty() ? nullptr : problem.params.data(), int32_t(problem.params.size())};
+  pode_prior pr{prior.nu, prior.dim, prior.sigma};
+  pode_ieks_config cfg{config.max_iterations, config.traj_rtol, config.obj_atol, config.obj_rtol,
+                       config.linearization == Linearization::kEk0 ? 1 : 0};
+  std::vector<double> means(size_t(cnt) * D), cov(size_t(cnt) * D * D), sm(size_t(cnt) * d), sc(size_t(cnt) * d * d);
+  std::vector<double> trace(size_t(std::max(config.max_iterations, 1)));
+  pode_ieks_report rep{means.data(), cov.data(), sm.data(), sc.data(), trace.data(), int32_t(trace.size()),
+                       PODE_HOST, 0, 0, 0.0, {0, 0}};
+  pode_shard_comm comm{rank, ranks, allgather, user};
+  pode_status st{};
+  check(pode_ieks_sharded(dev.handle(), &p, &pr, grid.data(), n1, &cfg, &comm, &rep, &st), st);
+  SolverReport<Matrix, Vector> out;
+  out.times.assign(grid.begin() + first, grid.begin() + first + cnt);
+  out.marginals.resize(size_t(cnt));
+  out.solution_means.resize(size_t(cnt));
+  out.solution_covs.resize(size_t(cnt));
+  for (int64_t n = 0; n < cnt; ++n) {
+    out.marginals[n] = {detail::getv<Vector>(means.data() + n * D, D),
+                        detail::get<Matrix>(cov.data() + n * D * D, D, D)};
+    out.solution_means[n] = detail::getv<Vector>(sm.data() + n * d, d);
+    out.solution_covs[n] = detail::get<Matrix>(sc.data() + n * d * d, d, d);
+  }
+  out.sigma_hat = rep.sigma_hat;
+  out.iterations = rep.iterations;
+  out.objective_trace.assign(trace.begin(), trace.begin() + rep.iterations);
+  out.converged = rep.converged != 0;
+  out.scan_stats.combine_invocations = std::size_t(rep.scan_stats.combine_invocations);
+  out.scan_stats.sequential_depth = std::size_t(rep.scan_stats.sequential_depth);
+  return out;
+}
+
 }  // namespace b200
 }  // namespace paraode

@@ -132,6 +132,29 @@ int main() {
     CHECK(res.stats.combine_invocations > 0);
   }
 
+  // one-shard para_ieks_sharded (identity all-gather) = para_ieks
+  {
+    pb::Problem p;
+    p.kind = PODE_VAN_DER_POL;
+    p.dim = 2;
+    p.t_end = 6.3;
+    p.y0 = {2.0, 0.0};
+    std::vector<double> grid(101);
+    for (int n = 0; n <= 100; ++n) grid[n] = 6.3 * n / 100.0;
+    const pb::IwpPrior prior{2, 2, 1.0};
+    auto a = pb::para_ieks<Mat, Vec>(p, prior, grid, pb::IeksConfig{}, gpu);
+    pode_allgather_fn same = [](void*, const double* send, int64_t count, double* recv) -> int {
+      for (int64_t i = 0; i < count; ++i) recv[i] = send[i];
+      return 0;
+    };
+    auto b = pb::para_ieks_sharded<Mat, Vec>(p, prior, grid, pb::IeksConfig{}, 0, 1, same, nullptr, gpu);
+    CHECK(b.iterations == a.iterations && b.marginals.size() == a.marginals.size());
+    double worst = 0.0;
+    for (size_t n = 0; n < a.marginals.size(); ++n)
+      for (int k = 0; k < 6; ++k) worst = std::fmax(worst, std::fabs(a.marginals[n].mean[k] - b.marginals[n].mean[k]));
+    CHECK(worst <= 1e-12);
+  }
+
   std::printf("%s (%d failures)\n", failures ? "FAIL" : "PASS", failures);
   return failures ? 1 : 0;
 }
