@@ -487,6 +487,47 @@ def para_ieks(ivp: InitialValueProblem, prior: IwpPrior, grid: Sequence[float],
                         rep.scan_stats.combine_invocations, rep.scan_stats.sequential_depth)
 
 
+# ---------------------------------------------------- batched solves ---
+_batch_ctxs: list = []
+
+
+def para_ieks_batch(problems: Sequence[InitialValueProblem], prior: IwpPrior, grid: Sequence[float],
+                    config: IeksConfig = IeksConfig(), want_cov=True, streams: int = 8, device: int = 0):
+    """Independent IVP solves (e.g. a parameter or initial-value sweep)
+    running concurrently: `streams` host threads, each driving its own
+    context (CUDA stream + workspace) through para_ieks, so small-N solves —
+    latency-bound one at a time — overlap on the GPU.  Returns the reports
+    in input order; each equals the single para_ieks call bit for bit
+    (SURVEY.md §8(f) item 4)."""
+    import threading
+    problems = list(problems)
+    if not problems:
+        return []
+    streams = max(1, min(int(streams), len(problems)))
+    while len(_batch_ctxs) < streams:
+        _batch_ctxs.append(Context(device))
+    out = [None] * len(problems)
+    errors = []
+
+    def worker(w):
+        ctx = _batch_ctxs[w]
+        for i in range(w, len(problems), streams):
+            try:
+                out[i] = para_ieks(problems[i], prior, grid, config, want_cov=want_cov, ctx=ctx)
+            except Exception as e:  # re-raised on the caller's thread
+                errors.append((i, e))
+                return
+
+    threads = [threading.Thread(target=worker, args=(w,)) for w in range(streams)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise min(errors, key=lambda x: x[0])[1]
+    return out
+
+
 # ------------------------------------------------ time-axis sharding ---
 def shard_range(n_nodes: int, rank: int, ranks: int):
     """(first node, reported node count) of shard `rank` (pode_shard_range)."""

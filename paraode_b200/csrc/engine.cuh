@@ -11,6 +11,7 @@
 #pragma once
 
 #include <algorithm>
+#include <mutex>
 #include <cstdlib>
 #include <vector>
 
@@ -20,6 +21,22 @@
 namespace pode {
 
 constexpr int kWarpsPerBlock = 4;
+
+// Runs a function-attribute setup once per device, thread-safe (several
+// host threads may drive their own contexts concurrently).
+struct OncePerDevice {
+  std::mutex m;
+  unsigned long long done = 0;
+  template <class F>
+  void operator()(F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(m);
+    if ((done >> dev) & 1ull) return;
+    f();
+    done |= 1ull << dev;
+  }
+};
 constexpr int kThreads = 32 * kWarpsPerBlock;
 
 struct FEd {  // device filtering-element arrays
@@ -589,9 +606,10 @@ struct Engine {
   }
 
   static void set_smem() {
-    static bool done = false;
-    if (done) return;
-    done = true;
+    static OncePerDevice once;
+    once([] { set_smem_now(); });
+  }
+  static void set_smem_now() {
     const int bytes = static_cast<int>(smem_bytes<D>());
     cudaFuncSetAttribute(k_combine<D, FOps<D>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(k_combine<D, SOps<D>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -648,13 +666,12 @@ struct Engine {
     if (level >= 1 && n <= bscan_max()) {  // block Sklansky levels
       constexpr int G = bscan_groups<D>();
       sm = bscan_smem<D, FOps<D>>();
-      static bool attr = false;
-      if (!attr) {
-        attr = true;
+      static OncePerDevice once;
+      once([&] {
         cuda_check(cudaFuncSetAttribute(k_bscan_loc<D, FTOps<D>, false>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)),
                    "bscan smem");
-      }
+      });
       const int64_t nb = (n + G - 1) / G;
       FEd agg = alloc<FOps<D>>(ctx, "gscan_agg_" + std::to_string(level), nb);
       k_bscan_loc<D, FTOps<D>, false><<<unsigned(nb), kBWarps * 32, sm, ctx->stream>>>(in, n, nb == 1 ? out : loc,
@@ -701,13 +718,12 @@ struct Engine {
 
   static ScanTally scan_filtering_gauss(pode_context* ctx, int64_t n, FEd in, FEd out, int L) {
     set_smem();
-    static bool attr = false;
-    if (!attr) {
-      attr = true;
+    static OncePerDevice once;
+    once([&] {
       const int bytes = static_cast<int>(smem_bytes<D>());
       cudaFuncSetAttribute(k_scan_reduce_loc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
       cudaFuncSetAttribute(k_scan_down_gauss<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    }
+    });
     ScanTally t;
     if (n >= 1) scan_gauss_rec(ctx, in, out, n, 0, L, t);
     return t;
@@ -721,13 +737,12 @@ struct Engine {
     if (level >= 1 && n <= bscan_max()) {  // block Sklansky levels
       constexpr int G = bscan_groups<D>();
       sm = bscan_smem<D, MOps<D>>();
-      static bool attr = false;
-      if (!attr) {
-        attr = true;
+      static OncePerDevice once;
+      once([&] {
         cuda_check(cudaFuncSetAttribute(k_bscan_loc<D, MOps<D>, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(sm)),
                    "bscan smem");
-      }
+      });
       const int64_t nb = (n + G - 1) / G;
       SEd agg = alloc<SOps<D>>(ctx, "mscan_agg_" + std::to_string(level), nb);
       k_bscan_loc<D, MOps<D>, true><<<unsigned(nb), kBWarps * 32, sm, ctx->stream>>>(in, n, nb == 1 ? out : loc,
@@ -768,13 +783,12 @@ struct Engine {
   }
 
   static ScanTally scan_means_terminal(pode_context* ctx, int64_t n, SEd io, int L) {
-    static bool attr = false;
-    if (!attr) {
-      attr = true;
+    static OncePerDevice once;
+    once([&] {
       const int bytes = static_cast<int>(smem_bytes<D>());
       cudaFuncSetAttribute(k_mscan_reduce_loc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
       cudaFuncSetAttribute(k_mscan_down<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    }
+    });
     ScanTally t;
     if (n >= 1) mscan_rec(ctx, io, io, n, 0, L, t);
     return t;

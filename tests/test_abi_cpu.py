@@ -63,6 +63,11 @@ def test_no_gpu_fails_loudly_without_fallback():
         P.Context(0)
     with pytest.raises(P.CudaError):
         P.para_ieks(P.logistic(), P.IwpPrior(1, 1, 1.0), P.uniform_grid(10.0, 16))
+    with pytest.raises(P.CudaError):
+        P.para_ieks_batch([P.logistic()] * 3, P.IwpPrior(1, 1, 1.0), P.uniform_grid(10.0, 16))
+    from paraode_b200.accuracy import rk4_table
+    with pytest.raises(P.CudaError):
+        rk4_table(P.rigid_body(), 64)
 
 
 def test_null_context_is_rejected():
