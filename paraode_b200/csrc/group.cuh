@@ -43,7 +43,12 @@ struct Scratch {
   static constexpr int kTile = 4 * D * D;
   // vector area: [0,D) factor inverse diagonal, [D,2D) gather slot,
   // [2D,3D) spare slot, [3D, 5D+2) LQ reflector.
-  static constexpr int kDoubles = kTile + 6 * D + 4;
+  static constexpr int kRaw = kTile + 6 * D + 4;
+  // Group stride = 1 (mod 16) doubles: the groups of a warp then start on
+  // distinct 2-word bank pairs, so the group-broadcast reads of mm/publish
+  // (every group reading its own tile) are one wavefront instead of up to
+  // three (ncu: ~50 % of shared-load wavefronts were bank conflicts).
+  static constexpr int kDoubles = kRaw + (17 - kRaw % 16) % 16;
 };
 
 template <int D>
