@@ -44,11 +44,12 @@ struct Scratch {
   // vector area: [0,D) factor inverse diagonal, [D,2D) gather slot,
   // [2D,3D) spare slot, [3D, 5D+2) LQ reflector.
   static constexpr int kRaw = kTile + 6 * D + 4;
-  // Group stride = 1 (mod 16) doubles: the groups of a warp then start on
-  // distinct 2-word bank pairs, so the group-broadcast reads of mm/publish
+  // Group stride = 2 (mod 16) doubles: the groups of a warp then start on
+  // distinct 4-word bank slots, so the group-broadcast reads of mm/publish
   // (every group reading its own tile) are one wavefront instead of up to
-  // three (ncu: ~50 % of shared-load wavefronts were bank conflicts).
-  static constexpr int kDoubles = kRaw + (17 - kRaw % 16) % 16;
+  // three (ncu: ~50 % of shared-load wavefronts were bank conflicts), and
+  // every tile stays 16-byte aligned for double2 rows.
+  static constexpr int kDoubles = kRaw + (18 - kRaw % 16) % 16;
 };
 
 template <int D>
@@ -75,13 +76,41 @@ struct Grp {
 __device__ __forceinline__ void wsync() { __syncwarp(); }
 
 // ----------------------------------------------------------- publishing ---
+// Tile rows of even length move as double2 (16-byte shared accesses; tiles
+// and row starts are 16-byte aligned then), odd ones element-wise.
+template <int K>
+__device__ __forceinline__ void st_tile_row(double* p, const Rw<K>& x) {
+  if constexpr (K % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < K / 2; ++j) reinterpret_cast<double2*>(p)[j] = make_double2(x[2 * j], x[2 * j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < K; ++j) p[j] = x[j];
+  }
+}
+template <int K>
+__device__ __forceinline__ Rw<K> ld_tile_row(const double* p) {
+  Rw<K> x;
+  if constexpr (K % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < K / 2; ++j) {
+      const double2 v = reinterpret_cast<const double2*>(p)[j];
+      x[2 * j] = v.x;
+      x[2 * j + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < K; ++j) x[j] = p[j];
+  }
+  return x;
+}
+
 // Writes this lane's row into the tile (row stride K) bracketed by warp
 // barriers: the leading one protects readers of the previous contents.
 template <int D, int K>
 __device__ __forceinline__ void publish(const Grp<D>& g, const Rw<K>& row) {
   wsync();
-#pragma unroll
-  for (int j = 0; j < K; ++j) g.sc[g.r * K + j] = row[j];
+  st_tile_row<K>(g.sc + g.r * K, row);
   wsync();
 }
 
@@ -89,11 +118,8 @@ __device__ __forceinline__ void publish(const Grp<D>& g, const Rw<K>& row) {
 template <int D, int K>
 __device__ __forceinline__ void publish2(const Grp<D>& g, const Rw<K>& a, const Rw<K>& b) {
   wsync();
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    g.sc[g.r * K + j] = a[j];
-    g.sc[(D + g.r) * K + j] = b[j];
-  }
+  st_tile_row<K>(g.sc + g.r * K, a);
+  st_tile_row<K>(g.sc + (D + g.r) * K, b);
   wsync();
 }
 
@@ -108,10 +134,7 @@ __device__ __forceinline__ void publish_vec(const Grp<D>& g, double x, int slot 
 template <int D>
 __device__ __forceinline__ Rw<D> gather_vec(const Grp<D>& g, double x) {
   publish_vec(g, x);
-  Rw<D> o;
-#pragma unroll
-  for (int k = 0; k < D; ++k) o[k] = g.vs[D + k];
-  return o;
+  return ld_tile_row<D>(g.vs + D);
 }
 
 // y = A x  (A rows on lanes, x distributed) -> y_r on lane r.
@@ -128,8 +151,7 @@ __device__ __forceinline__ double matvec(const Grp<D>& g, const Rw<D>& a, double
 template <int D>
 __device__ __forceinline__ double matvec_t(const Grp<D>& g, const Rw<D>& a, double x) {
   wsync();
-#pragma unroll
-  for (int j = 0; j < D; ++j) g.sc[g.r * D + j] = a[j];
+  st_tile_row<D>(g.sc + g.r * D, a);
   g.vs[D + g.r] = x;
   wsync();
   double acc = 0.0;
@@ -167,8 +189,9 @@ __device__ __forceinline__ Rw<K> mm(const Grp<D>& g, const Rw<D>& a, const Rw<K>
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     const double ak = a[k];
+    const Rw<K> bk = ld_tile_row<K>(g.sc + k * K);
 #pragma unroll
-    for (int j = 0; j < K; ++j) c[j] = fma(ak, g.sc[k * K + j], c[j]);
+    for (int j = 0; j < K; ++j) c[j] = fma(ak, bk[j], c[j]);
   }
   return c;
 }
@@ -180,9 +203,10 @@ __device__ __forceinline__ Rw<D> mm_nt(const Grp<D>& g, const Rw<D>& a, const Rw
   Rw<D> c;
 #pragma unroll
   for (int j = 0; j < D; ++j) {
+    const Rw<D> bj = ld_tile_row<D>(g.sc + j * D);
     double acc = 0.0;
 #pragma unroll
-    for (int k = 0; k < D; ++k) acc = fma(a[k], g.sc[j * D + k], acc);
+    for (int k = 0; k < D; ++k) acc = fma(a[k], bj[k], acc);
     c[j] = acc;
   }
   return c;
@@ -196,8 +220,9 @@ __device__ __forceinline__ Rw<D> mm_tn(const Grp<D>& g, const Rw<D>& a, const Rw
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     const double akr = g.sc[k * D + g.r];
+    const Rw<D> bk = ld_tile_row<D>(g.sc + (D + k) * D);
 #pragma unroll
-    for (int j = 0; j < D; ++j) c[j] = fma(akr, g.sc[(D + k) * D + j], c[j]);
+    for (int j = 0; j < D; ++j) c[j] = fma(akr, bk[j], c[j]);
   }
   return c;
 }
@@ -449,8 +474,7 @@ __device__ __forceinline__ Rw<D> sqrt_sum_lt(const Grp<D>& g, const Rw<D>& a, co
 template <int D, int K>
 __device__ __forceinline__ void publish_factor(const Grp<D>& g, const Rw<K>& l_row) {
   wsync();
-#pragma unroll
-  for (int j = 0; j < D; ++j) g.sc[g.r * D + j] = l_row[j];
+  st_tile_row<D>(g.sc + g.r * D, l_row);
   g.vs[g.r] = 1.0 / l_row[g.r];
   wsync();
 }
