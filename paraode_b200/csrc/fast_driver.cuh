@@ -131,6 +131,15 @@ struct FastEngine {
     return v >= 2 ? v : 4;
   }
 
+  static void set_attrs() {
+    static OncePerDevice once;
+    once([] {
+      cuda_check(cudaFuncSetAttribute(lane::k_lane_fwd_down<D, d, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(lane::fwd_down_smem<D>())),
+                 "pass C smem");
+    });
+  }
+
   // One chunk per thread, ~256 resident threads per SM.
   static int chunk_len(pode_context* ctx, int64_t N) {
     const char* env = std::getenv("PODE_CHUNK");  // unset or empty: the default below
@@ -144,8 +153,10 @@ struct FastEngine {
                         int64_t n1, const pode_ieks_config& cfg, double* means, double* cov, double* sol_m,
                         double* sol_c) {
     using IE = IeksEngine<D>;
+    set_attrs();
     IeksSetup<D> s;
-    IE::setup(ctx, p, prior, grid_h, n1, s);
+    const bool element_finalize = std::getenv("PODE_FINALIZE") && std::string(std::getenv("PODE_FINALIZE")) == "elements";
+    IE::setup(ctx, p, prior, grid_h, n1, s, element_finalize);
     cudaStream_t st = ctx->stream;
     Workspace& ws = ctx->ws;
     const int64_t N = s.N;
@@ -219,10 +230,9 @@ struct FastEngine {
       lane::k_lane_fwd_reduce<D, d><<<lblocks, th, 0, st>>>(ag, cst, agg);
       note_launch(ctx, "fast_fwd_reduce");
       const ScanTally tf = Engine<D>::scan_filtering_gauss(ctx, nc, agg, agg, scan_fanin());
-      lane::k_lane_fwd_down<D, d><<<lblocks, th, 0, st>>>(ag, cst, agg, soa);
+      lane::k_lane_fwd_down<D, d><<<lblocks, th, lane::fwd_down_smem<D>(), st>>>(ag, cst, agg, soa, nullptr,
+                                                                                nullptr, nullptr, bagg);
       note_launch(ctx, "fast_fwd_down");
-      lane::k_lane_bfold<D><<<lblocks, th, 0, st>>>(soa, N, L, nc, bagg);
-      note_launch(ctx, "fast_bwd_fold");
       const ScanTally tr = Engine<D>::scan_means_terminal(ctx, nc, bagg, scan_fanin());
       lane::k_lane_bwd_down<D, d, false><<<lblocks, th, 0, st>>>(ag, cst, soa, bagg, eta_a, term(eta_a), eta_b,
                                                                   term(eta_b), part);
@@ -263,7 +273,7 @@ struct FastEngine {
     eta_a = (it & 1) ? pair1 : pair0;
     eta_b = (it & 1) ? pair0 : pair1;
     res.iterations = it;
-    if (std::getenv("PODE_FINALIZE") && std::string(std::getenv("PODE_FINALIZE")) == "elements") {
+    if (element_finalize) {
       // row-major copies of the final linearisation point and trajectory
       double* lin_rows = ws.arr<double>("lane_lin_rows", size_t(n1) * D);
       double* out_rows = ws.arr<double>("lane_out_rows", size_t(n1) * D);
@@ -359,9 +369,10 @@ struct FastEngine {
                                 const pode_shard_comm& comm, double* means, double* cov, double* sol_m,
                                 double* sol_c) {
     using IE = IeksEngine<D>;
+    set_attrs();
     const int R = comm.ranks, rank = comm.rank;
     IeksSetup<D> s;
-    IE::setup(ctx, p, prior, grid_h, n1g, s);
+    IE::setup(ctx, p, prior, grid_h, n1g, s, false);
     cudaStream_t st = ctx->stream;
     Workspace& ws = ctx->ws;
     const int64_t Ng = s.N;
@@ -460,10 +471,9 @@ struct FastEngine {
       note_launch(ctx, "fast_fwd_reduce");
       forward_exchange();
       const ScanTally tf = Engine<D>::scan_filtering_gauss(ctx, nc, agg, agg, scan_fanin());
-      lane::k_lane_fwd_down<D, d><<<lblocks, th, 0, st>>>(a, cst, agg, soa);
+      lane::k_lane_fwd_down<D, d><<<lblocks, th, lane::fwd_down_smem<D>(), st>>>(a, cst, agg, soa, nullptr, nullptr,
+                                                                                nullptr, bagg);
       note_launch(ctx, "fast_fwd_down");
-      lane::k_lane_bfold<D><<<lblocks, th, 0, st>>>(soa, N, L, nc, bagg, a.last);
-      note_launch(ctx, "fast_bwd_fold");
       backward_exchange();
       const ScanTally tr = Engine<D>::scan_means_terminal(ctx, nc, bagg, scan_fanin());
       lane::k_lane_bwd_down<D, d, false><<<lblocks, th, 0, st>>>(a, cst, soa, bagg, eta_a, term(eta_a), eta_b,

@@ -305,8 +305,10 @@ struct IeksSetup {
 
 template <int D>
 struct IeksEngine {
+  // node_scales = false (fused engine): T_n is recomputed in the kernels, so
+  // only T_0 is needed, on the host — no scale arrays, no stream sync.
   static void setup(pode_context* ctx, const host::Problem& p, const pode_prior& prior, const double* grid_h,
-                    int64_t n1, IeksSetup<D>& s) {
+                    int64_t n1, IeksSetup<D>& s, bool node_scales = true) {
     s.nu = prior.nu;
     s.dim = prior.dim;
     s.n1 = n1;
@@ -315,10 +317,12 @@ struct IeksEngine {
     Workspace& ws = ctx->ws;
     s.grid = ws.arr<double>("ieks_grid", n1);
     cuda_check(cudaMemcpyAsync(s.grid, grid_h, sizeof(double) * n1, cudaMemcpyHostToDevice, st), "grid");
-    s.scale = ws.arr<double>("ieks_scale", n1 * D);
-    s.scale_inv = ws.arr<double>("ieks_scale_inv", n1 * D);
-    k_node_scales<<<grid1(n1), kRedThreads, 0, st>>>(s.grid, n1, s.nu, s.dim, s.scale, s.scale_inv);
-    note_launch(ctx, "node_scales");
+    if (node_scales) {
+      s.scale = ws.arr<double>("ieks_scale", n1 * D);
+      s.scale_inv = ws.arr<double>("ieks_scale_inv", n1 * D);
+      k_node_scales<<<grid1(n1), kRedThreads, 0, st>>>(s.grid, n1, s.nu, s.dim, s.scale, s.scale_inv);
+      note_launch(ctx, "node_scales");
+    }
     const std::vector<double> phibar = host::preconditioned_phi(s.nu, s.dim);
     s.h_qunit = host::preconditioned_q_sqrt(s.nu, s.dim);
     s.h_q = s.h_qunit;
@@ -341,8 +345,19 @@ struct IeksEngine {
     std::copy(mu0.begin(), mu0.end(), hc.begin() + 3 * D * D + D);
     cuda_check(cudaMemcpyAsync(c, hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice, st), "consts");
     std::vector<double> si0(D);
-    cuda_check(cudaMemcpyAsync(si0.data(), s.scale_inv, sizeof(double) * D, cudaMemcpyDeviceToHost, st), "si0");
-    cuda_check(cudaStreamSynchronize(st), "sync");
+    if (node_scales) {
+      cuda_check(cudaMemcpyAsync(si0.data(), s.scale_inv, sizeof(double) * D, cudaMemcpyDeviceToHost, st), "si0");
+      cuda_check(cudaStreamSynchronize(st), "sync");
+    } else {  // T_0^-1 from the first step (k_node_scales' formula, ieks.cpp:28-33)
+      const double h = grid_h[1] - grid_h[0], root_h = std::sqrt(h);
+      double fact = 1.0;
+      for (int i = s.nu; i >= 0; --i) {
+        const int k = s.nu - i;
+        if (k > 0) fact *= k;
+        const double tau = root_h * std::pow(h, double(k)) / fact;
+        for (int r = 0; r < s.dim; ++r) si0[r * (s.nu + 1) + i] = 1.0 / tau;
+      }
+    }
     s.h_m0.assign(D + D * D, 0.0);
     for (int k = 0; k < D; ++k) s.h_m0[k] = si0[k] * mu0[k];
     cuda_check(cudaMemcpyAsync(s.init_m, s.h_m0.data(), sizeof(double) * s.h_m0.size(), cudaMemcpyHostToDevice, st),

@@ -390,6 +390,12 @@ __device__ __forceinline__ void st_mat(double* p, const double (&m)[D][D]) {
     for (int j = 0; j < D; ++j) p[r * D + j] = m[r][j];
 }
 
+// Dynamic shared memory of pass C (the fused backward-aggregate slots).
+template <int D>
+constexpr size_t fwd_down_smem() {
+  return sizeof(double) * (D * D + D) * kLaneThreads;
+}
+
 // A D x D matrix per node in the chunk-interleaved layout of ElemSoA::e.
 template <int D>
 __device__ __forceinline__ void mat_st(double* base, int64_t nc, int64_t c, int64_t t, const double (&m)[D][D]) {
@@ -556,7 +562,8 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(const FastArgs
 // ieks.cpp:79-104) into one partial per block.
 template <int D, int d, bool kFinal>
 __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastConst<D>& cst, const FEd& prefix,
-                                                 const ElemSoA& elems, double* cf, double* cterm, int64_t c) {
+                                                 const ElemSoA& elems, double* cf, double* cterm, int64_t c,
+                                                 double* sacc, const SEd& bagg) {
   using M = Model<D, d>;
   constexpr int B = M::B;
   double innov = 0.0;
@@ -646,6 +653,40 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
       gk[r] = m[r] - acc;
     }
     soa_st<D>(elems, c, k - s, E, gk);
+    if constexpr (!kFinal) {
+      // pass C2 fused: the chunk's backward aggregate (E, g) <- (E E_k, E g_k + g)
+      // in time order (⊗_s on means, parallel.cpp:146-156), accumulated in
+      // this thread's shared-memory slots (same arithmetic as k_lane_bfold)
+      auto ae = [&](int r, int j) -> double& { return sacc[(r * D + j) * kLaneThreads + threadIdx.x]; };
+      auto ag = [&](int r) -> double& { return sacc[(D * D + r) * kLaneThreads + threadIdx.x]; };
+      if (k == s) {
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) ae(r, j) = E[r][j];
+          ag(r) = gk[r];
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+          double row[D], o[D], og = ag(r);
+#pragma unroll
+          for (int x = 0; x < D; ++x) {
+            row[x] = ae(r, x);
+            o[x] = 0.0;
+          }
+#pragma unroll
+          for (int x = 0; x < D; ++x) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) o[j] = fma(row[x], E[x][j], o[j]);
+            og = fma(row[x], gk[x], og);
+          }
+#pragma unroll
+          for (int j = 0; j < D; ++j) ae(r, j) = o[j];
+          ag(r) = og;
+        }
+      }
+    }
     // measurement update at node k+1
     double ylin[d];
     gather_y<D, d>(a, lp, c, k + 1 - s, k + 1, ylin);
@@ -683,6 +724,23 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
     for (int r = 0; r < D; ++r) elems.term[r] = m[r];
     if constexpr (kFinal) st_mat<D>(cterm, C);
   }
+  if constexpr (!kFinal) {  // store the backward aggregate (the last shard's last chunk absorbs the terminal)
+    const bool term = e == a.N && a.last;
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      double og = sacc[(D * D + r) * kLaneThreads + threadIdx.x];
+      if (term) {
+#pragma unroll
+        for (int x = 0; x < D; ++x) og = fma(sacc[(r * D + x) * kLaneThreads + threadIdx.x], m[x], og);
+      }
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const double v = sacc[(r * D + j) * kLaneThreads + threadIdx.x];
+        bagg.e[c * D * D + r * D + j] = term ? 0.0 : v;
+      }
+      bagg.g[c * D + r] = og;
+    }
+  }
   if (bad_lin >= 0) raise_error(a.err, bad_lin, kErrLinearization);
   if (bad_sing) raise_error(a.err, s, kErrSingular);
   return innov;
@@ -691,11 +749,13 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
 template <int D, int d, bool kFinal = false>
 __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(const FastArgs a, FastConst<D> cst, FEd prefix,
                                                                 ElemSoA elems, double* cf = nullptr,
-                                                                double* cterm = nullptr, double* part = nullptr) {
+                                                                double* cterm = nullptr, double* part = nullptr,
+                                                                SEd bagg = SEd{}) {
   __shared__ double red[kFinal ? kLaneThreads : 1];
+  extern __shared__ double sacc[];  // !kFinal: (D*D + D) x kLaneThreads aggregate slots
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   double innov = 0.0;
-  if (c < a.nchunks) innov = fwd_down_chunk<D, d, kFinal>(a, cst, prefix, elems, cf, cterm, c);
+  if (c < a.nchunks) innov = fwd_down_chunk<D, d, kFinal>(a, cst, prefix, elems, cf, cterm, c, sacc, bagg);
   if constexpr (kFinal) block_sum_partial(red, innov, part);  // every thread reaches the barriers
 }
 
