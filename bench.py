@@ -86,7 +86,8 @@ def kernel_model(D, d):
     fwd_down = phi * D + D * D * (D + 1) // 2 + f_lq(D, 2 * D, D) + D * D * D + D * D + phi + upd
     return {
         "fast_fwd_reduce": (2 * fwd_reduce, 8 * D),
-        "fast_fwd_down": (2 * fwd_down, 8 * (D + D * D + D)),
+        # pass C with the backward chunk aggregate (pass C2) fused in
+        "fast_fwd_down": (2 * (fwd_down + D ** 3 + D * D), 8 * (D + D * D + D)),
         "fast_bwd_fold": (2 * (D ** 3 + D * D), 8 * (D * D + D)),
         "fast_bwd_down": (2 * (D * D + phi + D * D // 2 + 2 * D), 8 * (D * D + D + 2 * D)),
     }
