@@ -351,6 +351,11 @@ void pode_context_destroy(pode_context* ctx) {
   if (ctx == nullptr) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto& kv : ctx->graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+  }
+  ctx->graphs.clear();
   for (auto& kv : ctx->ws.bufs)
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   ctx->ws.bufs.clear();

@@ -39,9 +39,11 @@ struct Workspace {
     size_t bytes = 0;
   };
   std::map<std::string, Buf> bufs;
+  uint64_t generation = 0;  // bumped on every (re)allocation: cached graphs hold raw pointers
   void* get(const std::string& tag, size_t bytes) {
     Buf& b = bufs[tag];
     if (b.bytes < bytes) {
+      ++generation;
       if (b.ptr) cudaFree(b.ptr);
       b.ptr = nullptr;
       b.bytes = 0;
@@ -80,6 +82,15 @@ struct pode_context {
   unsigned long long* h_err = nullptr;  // pinned mirror
   double* h_scalars = nullptr;          // pinned scalars (reductions)
   int64_t launches = 0;
+  // Instantiated device-side IEKS loops (fast_driver.cuh), reused while the
+  // captured kernel arguments (key) and the workspace generation match.
+  struct GraphSlot {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::string key;
+    int64_t per_iter = 0;
+  };
+  std::map<std::string, GraphSlot> graphs;
   // pinned staging ring for large device->host result copies (capi.cu)
   char* h_stage[2] = {nullptr, nullptr};
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};

@@ -78,40 +78,47 @@ struct FastEngine {
   }
 
   template <class Body>
+  // `key` serialises every argument the captured kernels see (plus the
+  // workspace generation): an identical key reuses the instantiated graph of
+  // an earlier solve on this context instead of capturing again.
   static void graph_loop(pode_context* ctx, const IeksSetup<D>& s, Body& body, LoopState* ls, double* trace_dev,
-                         int& it, double& v_prev, const pode_ieks_config& cfg, IeksResult& res) {
+                         int& it, double& v_prev, const pode_ieks_config& cfg, IeksResult& res,
+                         const std::string& key) {
     cudaStream_t st = ctx->stream;
     LoopState h0{it, 0, cfg.max_iterations, 0, v_prev, cfg.traj_rtol, cfg.obj_atol, cfg.obj_rtol};
     cuda_check(cudaMemcpyAsync(ls, &h0, sizeof(h0), cudaMemcpyHostToDevice, st), "loop state");
     reset_error(ctx);
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    cuda_check(cudaGraphCreate(&graph, 0), "graph");
-    cudaGraphConditionalHandle h;
-    cuda_check(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault), "cond handle");
-    cudaGraphNodeParams np = {};
-    np.type = cudaGraphNodeTypeConditional;
-    np.conditional.handle = h;
-    np.conditional.type = cudaGraphCondTypeWhile;
-    np.conditional.size = 1;
-    cudaGraphNode_t node;
-    cuda_check(cudaGraphAddNode(&node, graph, nullptr, 0, &np), "while node");
-    cudaGraph_t g_body = np.conditional.phGraph_out[0];
-    const int64_t l0 = ctx->launches;
-    cuda_check(cudaStreamBeginCaptureToGraph(st, g_body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed),
-               "capture");
-    body(true, h);
-    cuda_check(cudaStreamEndCapture(st, &g_body), "end capture");
-    const int64_t per_iter = ctx->launches - l0;
-    ctx->launches = l0;
-    cuda_check(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
-    cuda_check(cudaGraphLaunch(exec, st), "graph launch");
+    pode_context::GraphSlot& slot = ctx->graphs["ieks_" + std::to_string(D) + "_" + std::to_string(d)];
+    if (slot.exec == nullptr || slot.key != key) {
+      if (slot.exec) cudaGraphExecDestroy(slot.exec);
+      if (slot.graph) cudaGraphDestroy(slot.graph);
+      slot = pode_context::GraphSlot{};
+      cuda_check(cudaGraphCreate(&slot.graph, 0), "graph");
+      cudaGraphConditionalHandle h;
+      cuda_check(cudaGraphConditionalHandleCreate(&h, slot.graph, 1, cudaGraphCondAssignDefault), "cond handle");
+      cudaGraphNodeParams np = {};
+      np.type = cudaGraphNodeTypeConditional;
+      np.conditional.handle = h;
+      np.conditional.type = cudaGraphCondTypeWhile;
+      np.conditional.size = 1;
+      cudaGraphNode_t node;
+      cuda_check(cudaGraphAddNode(&node, slot.graph, nullptr, 0, &np), "while node");
+      cudaGraph_t g_body = np.conditional.phGraph_out[0];
+      const int64_t l0 = ctx->launches;
+      cuda_check(cudaStreamBeginCaptureToGraph(st, g_body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed),
+                 "capture");
+      body(true, h);
+      cuda_check(cudaStreamEndCapture(st, &g_body), "end capture");
+      slot.per_iter = ctx->launches - l0;
+      ctx->launches = l0;
+      cuda_check(cudaGraphInstantiate(&slot.exec, slot.graph, 0), "instantiate");
+      slot.key = key;
+    }
+    cuda_check(cudaGraphLaunch(slot.exec, st), "graph launch");
     LoopState hs;
     cuda_check(cudaMemcpyAsync(&hs, ls, sizeof(hs), cudaMemcpyDeviceToHost, st), "loop state");
-    const unsigned long long key = fetch_error(ctx);  // syncs
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
-    ctx->launches += per_iter * (hs.it - it);
+    const unsigned long long ekey = fetch_error(ctx);  // syncs
+    ctx->launches += slot.per_iter * (hs.it - it);
     std::vector<double> tr(size_t(hs.it), 0.0);
     if (hs.it > it)
       cuda_check(cudaMemcpy(tr.data() + it, trace_dev + it, sizeof(double) * (hs.it - it), cudaMemcpyDeviceToHost),
@@ -120,8 +127,18 @@ struct FastEngine {
     it = hs.it;
     v_prev = hs.v_prev;
     res.converged = hs.converged != 0;
-    if (key != ~0ull) IeksEngine<D>::check_linearization(ctx, s, it);  // throws
+    if (ekey != ~0ull) IeksEngine<D>::check_linearization(ctx, s, it);  // throws
   }
+
+  // Byte key of the values a captured iteration depends on.
+  struct KeyWriter {
+    std::string k;
+    template <class T>
+    KeyWriter& operator<<(const T& v) {
+      k.append(reinterpret_cast<const char*>(&v), sizeof(T));
+      return *this;
+    }
+  };
 
   // Chunk-aggregate scans run on the group engine (engine.cuh): a lane-serial
   // ⊗_f needs ~250 live doubles per thread and spills.
@@ -249,7 +266,15 @@ struct FastEngine {
     };
     while (it < cfg.max_iterations) {
       if (it == 1 && use_graph(ctx, cfg)) {  // workspaces exist after one eager iteration
-        graph_loop(ctx, s, body, ls, trace_dev, it, v_prev, cfg, res);
+        KeyWriter kw;
+        kw << ctx->ws.generation << N << L << nc << padded << cfg.linearization << scan_fanin() << bscan_max()
+           << a.grid << a.err << a.prob.kind << a.prob.dim << pair0 << pair1 << agg.a << agg.b << agg.c << agg.eta
+           << agg.j << soa.e << soa.g << soa.term << bagg.e << bagg.g << part << nparts << ls << trace_dev
+           << ctx->d_err;
+        for (int k = 0; k < kMaxParams; ++k) kw << a.prob.params[k];
+        for (int k = 0; k < D * D; ++k) kw << cst.q[k] << cst.qunit[k];
+        for (int k = 0; k < D; ++k) kw << cst.qunit_rdiag[k] << cst.m0[k];
+        graph_loop(ctx, s, body, ls, trace_dev, it, v_prev, cfg, res, kw.k);
         if (res.converged || it >= cfg.max_iterations) break;
         continue;  // unreachable: the device loop runs to convergence or the budget
       }
