@@ -1100,6 +1100,22 @@ __global__ void __launch_bounds__(kLaneThreads, kBwdMinBlocks) k_lane_bwd_down(F
 #pragma unroll
         for (int r = 0; r < D; ++r) on[r] = eta_old[((k - 1 - s) * D + r) * nc + c];
       }
+      if (!kInitial && k - 2 >= s) {
+        // L2 prefetch of step k-2 for the whole warp (its 32 chunks span <= 3
+        // lines per entry), so the register prefetch above hits L2: more
+        // loads in flight without more registers.
+        constexpr int X = D * D + 2 * D;
+        const int lane = threadIdx.x & 31;
+        const int64_t cw = c - lane, t2 = k - 2 - s;
+        for (int q = lane; q < 3 * X; q += 32) {
+          const int x = q / 3, part = q - 3 * (q / 3);
+          const int64_t cc = min(nc - 1, cw + (part == 0 ? 0 : (part == 1 ? 16 : 31)));
+          const double* addr = x < D * D ? elems.e + (t2 * D * D + x) * nc + cc
+                                         : (x < D * D + D ? elems.g + (t2 * D + (x - D * D)) * nc + cc
+                                                          : eta_old + (t2 * D + (x - D * D - D)) * nc + cc);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(addr));
+        }
+      }
       double tk[B], tki[B];
       M::taus(a.grid, a.first, k, tk, tki);
       double etak[D];
