@@ -119,22 +119,23 @@ struct Model {
       for (int i = 0; i < B; ++i) pc[a][i] = (i >= a) ? binom(q - a, i - a) * ratio[i] : 0.0;
   }
 
-  // y = phi x (in place safe: row a of a block reads rows >= a).
-  template <int K>
+  // y = phi x on columns [0, NC) (in place safe: row a of a block reads
+  // rows >= a).
+  template <int K, int NC = K>
   __device__ static void phi_rows(const double (&pc)[B][B], double (&x)[D][K]) {
 #pragma unroll
     for (int blk = 0; blk < d; ++blk)
 #pragma unroll
       for (int a = 0; a < B; ++a) {
-        double o[K];
+        double o[NC];
 #pragma unroll
-        for (int j = 0; j < K; ++j) o[j] = pc[a][a] * x[blk * B + a][j];
+        for (int j = 0; j < NC; ++j) o[j] = pc[a][a] * x[blk * B + a][j];
 #pragma unroll
         for (int i = a + 1; i < B; ++i)
 #pragma unroll
-          for (int j = 0; j < K; ++j) o[j] = fma(pc[a][i], x[blk * B + i][j], o[j]);
+          for (int j = 0; j < NC; ++j) o[j] = fma(pc[a][i], x[blk * B + i][j], o[j]);
 #pragma unroll
-        for (int j = 0; j < K; ++j) x[blk * B + a][j] = o[j];
+        for (int j = 0; j < NC; ++j) x[blk * B + a][j] = o[j];
       }
   }
 
@@ -280,18 +281,8 @@ struct Model {
         m[r][j] = c[r][j];
         m[r][D + j] = qrow[r * D + j];
       }
-    // phi acts on the left half
-    double left[D][D];
-#pragma unroll
-    for (int r = 0; r < D; ++r)
-#pragma unroll
-      for (int j = 0; j < D; ++j) left[r][j] = m[r][j];
-    phi_rows<D>(pc, left);
-#pragma unroll
-    for (int r = 0; r < D; ++r)
-#pragma unroll
-      for (int j = 0; j < D; ++j) m[r][j] = left[r][j];
-    lq<D, 2 * D, D, D>(m);  // right block Q^1/2: lower triangular
+    phi_rows<2 * D, D>(pc, m);  // phi acts on the left half only
+    lq<D, 2 * D, D, D>(m);      // right block Q^1/2: lower triangular
 #pragma unroll
     for (int r = 0; r < D; ++r)
 #pragma unroll
