@@ -508,7 +508,7 @@ struct FastEngine {
       note_launch(ctx, "finish3");
       const unsigned long long key = fetch_error(ctx);
       gather3(ctx, comm, red, r3, any_failed, key != ~0ull);
-      if (key != ~0ull) IE::check_linearization(ctx, s, it);  // throws this shard's error
+      if (key != ~0ull) IE::check_linearization(ctx, s, it, g0);  // throws this shard's error
       if (any_failed) throw ApiError(PODE_ERR_SINGULAR_FACTOR, "ieks_sharded: another shard failed", 0, 0.0, it);
       res.stats.combines = std::max(res.stats.combines, (Ng - nc * R) + tf.combines * R + Ng);
       res.stats.depth = std::max(res.stats.depth, int64_t(L) + tf.depth + int64_t(L) + tr.depth + 2 * R);
@@ -538,7 +538,7 @@ struct FastEngine {
     {
       const unsigned long long key = fetch_error(ctx);
       gather3(ctx, comm, red, r3, any_failed, key != ~0ull);
-      if (key != ~0ull) IE::check_linearization(ctx, s, it);
+      if (key != ~0ull) IE::check_linearization(ctx, s, it, g0);
       if (any_failed) throw ApiError(PODE_ERR_SINGULAR_FACTOR, "ieks_sharded: another shard failed", 0, 0.0, it);
     }
     const double innov = r3[0];
@@ -567,7 +567,7 @@ struct FastEngine {
     lane::k_lane_fin_bwd<D, d><<<lblocks, th, 0, st>>>(a, cst, soa, cf, cterm, sagg, eta_a, term(eta_a), red, count,
                                                        lane::FinOut{means, cov, sol_m, sol_c});
     note_launch(ctx, "fin_bwd");
-    IE::check_linearization(ctx, s, it);  // syncs
+    IE::check_linearization(ctx, s, it, g0);  // syncs
     res.sigma_hat = std::sqrt(innov / count) * prior.sigma;
     return res;
   }

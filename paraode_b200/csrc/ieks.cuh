@@ -401,11 +401,12 @@ struct IeksEngine {
     check_linearization(ctx, s, it);
   }
 
-  static void check_linearization(pode_context* ctx, const IeksSetup<D>& s, int it) {
+  // node_offset: global index of local node 0 (time-axis shards).
+  static void check_linearization(pode_context* ctx, const IeksSetup<D>& s, int it, int64_t node_offset = 0) {
     const unsigned long long key = fetch_error(ctx);
     if (key == ~0ull) return;
     const int code = int(key & 0xff);
-    const int64_t idx = int64_t(key >> 8);
+    const int64_t idx = int64_t(key >> 8) + node_offset;
     if (code == kErrLinearization) {
       double t = 0.0;
       cuda_check(cudaMemcpy(&t, s.grid + idx, sizeof(double), cudaMemcpyDeviceToHost), "t");

@@ -25,8 +25,8 @@ namespace pode {
 namespace lane {
 
 constexpr int kLaneThreads = 128;
-// The streaming backward passes (C2, E) are HBM-bound: more resident warps
-// keep more loads in flight (register cap 64K / (128 * kBwdMinBlocks)).
+// Pass E is HBM-bound: more resident warps would keep more loads in flight
+// (register cap 64K / (128 * kBwdMinBlocks)); 3 and 4 spilled, so 2.
 #ifndef PODE_BWD_MIN_BLOCKS
 #define PODE_BWD_MIN_BLOCKS 2
 #endif
@@ -647,7 +647,7 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
     if constexpr (!kFinal) {
       // pass C2 fused: the chunk's backward aggregate (E, g) <- (E E_k, E g_k + g)
       // in time order (⊗_s on means, parallel.cpp:146-156), accumulated in
-      // this thread's shared-memory slots (same arithmetic as k_lane_bfold)
+      // this thread's shared-memory slots
       auto ae = [&](int r, int j) -> double& { return sacc[(r * D + j) * kLaneThreads + threadIdx.x]; };
       auto ag = [&](int r) -> double& { return sacc[(D * D + r) * kLaneThreads + threadIdx.x]; };
       if (k == s) {
@@ -748,54 +748,6 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(const FastArgs a
   double innov = 0.0;
   if (c < a.nchunks) innov = fwd_down_chunk<D, d, kFinal>(a, cst, prefix, elems, cf, cterm, c, sacc, bagg);
   if constexpr (kFinal) block_sum_partial(red, innov, part);  // every thread reaches the barriers
-}
-
-// Pass C2: one thread per chunk folds the chunk's smoothing elements in time
-// order into its backward aggregate, (E, g) <- (E E_n, E g_n + g)
-// (⊗_s on means, parallel.cpp:146-156); the last chunk includes the
-// terminal node N, so its aggregate has E = 0.
-template <int D>
-__global__ void __launch_bounds__(kLaneThreads, kBwdMinBlocks) k_lane_bfold(ElemSoA elems, int64_t N, int L, int64_t nchunks,
-                                                             SEd bagg, int terminal = 1) {
-  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (c >= nchunks) return;
-  const int64_t s = c * L;
-  const int64_t e = min(N, s + L);
-  const bool last = c == nchunks - 1 && terminal;
-  double Eg[D][D], gg[D];
-  soa_ld<D>(elems, c, 0, Eg, gg);
-  for (int64_t k = s + 1; k <= e; ++k) {
-    double E[D][D], gk[D];
-    if (k < e) {
-      soa_ld<D>(elems, c, k - s, E, gk);
-    } else {  // node e: only the terminal node N belongs to this chunk
-      if (!last) break;
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        gk[r] = elems.term[r];
-#pragma unroll
-        for (int j = 0; j < D; ++j) E[r][j] = 0.0;
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < D; ++r) {
-      double o[D], og = gg[r];
-#pragma unroll
-      for (int j = 0; j < D; ++j) o[j] = 0.0;
-#pragma unroll
-      for (int x = 0; x < D; ++x) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) o[j] = fma(Eg[r][x], E[x][j], o[j]);
-        og = fma(Eg[r][x], gk[x], og);
-      }
-#pragma unroll
-      for (int j = 0; j < D; ++j) Eg[r][j] = o[j];
-      gg[r] = og;
-    }
-  }
-  st_mat<D>(bagg.e + c * D * D, Eg);
-#pragma unroll
-  for (int r = 0; r < D; ++r) bagg.g[c * D + r] = gg[r];
 }
 
 // ------------------------------------------------- finalize (once) ---
