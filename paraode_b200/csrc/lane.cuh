@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(const FastArgs
     double cm[D][D];
     M::predict_cov(pc, C, cst.q, cm);
     // update at node k+1
-    double ylin[d];
+    double ylin[d];  // (a one-step-ahead load costs pass A more in spills than it saves)
     gather_y<D, d>(a, lp, c, k + 1 - s, k + 1, ylin);
     const typename M::Lin lin = M::linearize(a.prob, ylin, a.ek0);
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
@@ -582,6 +582,10 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
   M::taus(a.grid, a.first, s, tk, tki);
   bool bad_sing = false;
   int64_t bad_lin = -1;
+  // the linearisation point of the next step is loaded one step ahead, so
+  // its global-memory latency overlaps the current step's arithmetic
+  double ynext[d];
+  gather_y<D, d>(a, lp, c, 1, s + 1, ynext);
   for (int64_t k = s; k < e; ++k) {
     double tn[B], tni[B], ratio[B], pc[B][B];
     M::taus(a.grid, a.first, k + 1, tn, tni);
@@ -680,7 +684,9 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
     }
     // measurement update at node k+1
     double ylin[d];
-    gather_y<D, d>(a, lp, c, k + 1 - s, k + 1, ylin);
+#pragma unroll
+    for (int i = 0; i < d; ++i) ylin[i] = ynext[i];
+    if (k + 1 < e) gather_y<D, d>(a, lp, c, k + 2 - s, k + 2, ynext);
     const typename M::Lin lin = M::linearize(a.prob, ylin, a.ek0);
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
     const typename M::Upd u = M::update(lin, tn, cm);
