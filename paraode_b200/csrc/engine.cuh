@@ -500,6 +500,7 @@ struct FTOps : FOps<D> {
 // aggregate in agg[blockIdx.x] — the same contract as k_scan_reduce_loc with
 // chunk length G, so the one-combine-deep down-sweeps are unchanged.
 constexpr int kBWarps = 8;
+static_assert((kBWarps & (kBWarps - 1)) == 0, "k_bscan_loc puts the warp index in the low position bits");
 
 template <int D>
 constexpr int bscan_groups() {
