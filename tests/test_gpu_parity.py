@@ -351,3 +351,25 @@ def test_batch_parameter_sweep_matches_oracle():
         want = O.ieks(op, 2, O.uniform_grid(6.3, 200), mode=0)
         assert g.iterations == want["iterations"]
         assert rel(g.means, want["means"]) <= 1e-9
+
+
+def test_full_size_fhn_properties():
+    """BASELINE.json's headline size (FHN, IWP(2), N = 2^20), where the
+    sequential oracle is too slow to run: size-independent properties —
+    convergence, bitwise determinism of the whole solve, the posterior mean
+    against an RK4 solution on the same nodes (GPU, pode_rk4_table), and
+    calibrated covariances that are finite and positive on the diagonal."""
+    from paraode_b200.accuracy import rk4_table
+    prob = P.fitzhugh_nagumo()
+    n = 2 ** 20
+    grid = P.uniform_grid(prob.t_end, n)
+    a = P.para_ieks(prob, P.IwpPrior(2, 2, 1.0), grid)
+    b = P.para_ieks(prob, P.IwpPrior(2, 2, 1.0), grid)
+    assert a.converged and a.iterations == b.iterations
+    assert np.array_equal(a.means, b.means) and np.array_equal(a.cov_sqrt, b.cov_sqrt)
+    ref = rk4_table(prob, n)  # same nodes: no interpolation error
+    err = float(np.sqrt(np.mean((a.solution_means - ref) ** 2)))
+    print(f"N=2^20: iterations {a.iterations}, RMSE vs RK4 {err:.3e}, sigma_hat {a.sigma_hat:.3e}")
+    assert err <= 1e-9  # measured 1.0e-11
+    var = np.diagonal(a.solution_covs, axis1=1, axis2=2)
+    assert np.all(np.isfinite(a.cov_sqrt)) and np.all(var[1:] > 0.0)
