@@ -215,6 +215,7 @@ def run_reference(args):
         return
     threads = os.cpu_count() or 1
     n = CPU_SAMPLE_N
+    dim = {"logistic": 1, "fhn": 2, "vanderpol": 2, "rigidbody": 3}.get(args.problem, 2)
     for _ in range(max(0, min(args.warmup, 1))):
         cpu_solve(args.problem, args.nu, n, threads)
     times, iters = [], 0
@@ -226,10 +227,13 @@ def run_reference(args):
     sample = f"para_ieks on WorkPool({threads}), full solve at N={n} ({iters} iterations)"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "time-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.problem} d=2 IWP(q={args.nu}) D=6 IEKS to the reference stopping rule",
+            "scaling": "strong" if world > 1 and args.mode != "replicas" else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.problem} d={dim} IWP(q={args.nu}) D={dim * (args.nu + 1)}, "
+                                   f"N=2^{args.log2n} uniform steps, IEKS to the reference stopping rule",
                        "N": n, "iterations": iters,
-                       "note": "bounded sample at reduced N; the N=2^20 solve takes tens of minutes on CPU"},
+                       "note": f"bounded sample: full solves at N={n}; the N=2^{args.log2n} solve takes tens of "
+                               "minutes on CPU"},
             "cpu_baseline": {"value": v, "unit": "time-steps/s", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "time-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
