@@ -225,6 +225,16 @@ int pode_ieks(pode_context* ctx, const pode_problem* problem, const pode_prior* 
               const double* grid, int64_t n_nodes, const pode_ieks_config* config,
               pode_ieks_report* report, pode_status* status);
 
+/* Replaces eks_solve (proj/include/paraode/ieks.hpp:103-105, ieks.cpp:224-291):
+ * one forward pass linearised at each step's own predicted mean (sequential
+ * in time: one warp on the device), the smoother of those filtered
+ * marginals (reverse scan), calibration and outputs.  The report has
+ * iterations = 1, converged = 1 and a one-entry objective trace.
+ * linearization: 0 = EK1, 1 = EK0. */
+int pode_eks(pode_context* ctx, const pode_problem* problem, const pode_prior* prior,
+             const double* grid, int64_t n_nodes, int32_t linearization,
+             pode_ieks_report* report, pode_status* status);
+
 /* Accuracy reference of the benchmark harness (problems.cpp:11-27): `steps`
  * classical RK4 steps of the registered field on [0, t_end]; table holds
  * (steps+1) * dim host doubles.  PODE_ERR_INVALID_INPUT if it diverges. */

@@ -97,6 +97,8 @@ SYMBOLS = {
                            C.POINTER(Status)]),
     "pode_ieks": (C.c_int, [C.c_void_p, C.POINTER(Problem), C.POINTER(Prior), dptr, C.c_int64,
                             C.POINTER(IeksConfig), C.POINTER(IeksReport), C.POINTER(Status)]),
+    "pode_eks": (C.c_int, [C.c_void_p, C.POINTER(Problem), C.POINTER(Prior), dptr, C.c_int64, C.c_int32,
+                           C.POINTER(IeksReport), C.POINTER(Status)]),
     "pode_rk4_table": (C.c_int, [C.c_void_p, C.POINTER(Problem), C.c_int64, dptr, C.POINTER(Status)]),
     "pode_shard_range": (None, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "pode_ieks_sharded": (C.c_int, [C.c_void_p, C.POINTER(Problem), C.POINTER(Prior), dptr, C.c_int64,

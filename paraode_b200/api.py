@@ -487,6 +487,31 @@ def para_ieks(ivp: InitialValueProblem, prior: IwpPrior, grid: Sequence[float],
                         rep.scan_stats.combine_invocations, rep.scan_stats.sequential_depth)
 
 
+def eks_solve(ivp: InitialValueProblem, prior: IwpPrior, grid: Sequence[float], linearization: str = "ek1",
+              want_cov=True, ctx=None) -> SolverReport:
+    """Non-iterated extended Kalman smoother on the B200 (eks_solve,
+    ieks.cpp:224-291): each step is linearised at its own predicted mean in
+    one sequential forward pass (one warp), then smoothed by the reverse scan
+    and calibrated.  iterations = 1, converged = True."""
+    c = _ctx(ctx)
+    grid = _f64(grid)
+    n1 = grid.shape[0]
+    D, d = prior.state_dim, prior.dim
+    means = _result_array((n1, D))
+    cov = _result_array((n1, D, D)) if want_cov else None
+    sm = _result_array((n1, d))
+    sc = _result_array((n1, d, d)) if want_cov else None
+    trace = np.zeros(1)
+    rep = A.IeksReport(_p(means), _p(cov), _p(sm), _p(sc), _p(trace), 1, A.PODE_HOST, 0, 0, 0.0, A.ScanStats())
+    pr = ivp._c()
+    prior_c = A.Prior(prior.nu, prior.dim, prior.sigma)
+    st = A.Status()
+    _raise(c._lib.pode_eks(c.handle, C.byref(pr), C.byref(prior_c), _p(grid), n1,
+                           {"ek1": 0, "ek0": 1}[linearization], C.byref(rep), C.byref(st)), st)
+    return SolverReport(grid.copy(), means, cov, sm, sc, rep.sigma_hat, rep.iterations, trace.copy(),
+                        bool(rep.converged), rep.scan_stats.combine_invocations, rep.scan_stats.sequential_depth)
+
+
 # ---------------------------------------------------- batched solves ---
 _batch_ctxs: list = []
 

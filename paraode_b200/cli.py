@@ -12,9 +12,10 @@
   when means agree to --tolerance with equal iteration counts
   (bench.cpp:290-318); exit 0 all pass, 1 otherwise.
 
-Methods: `paraieks` (the fused engine) and `paraieks-elements` (element
-engine).  The reference's sequential CPU baselines `ieks` / `eks` are not
-part of the B200 path and are rejected as unknown methods.
+Methods: `paraieks` (the fused engine), `paraieks-elements` (element
+engine) and `eks` (the non-iterated smoother, eks_solve, on the device).
+The reference's sequential CPU `ieks` baseline is not part of the B200 path
+and is rejected as an unknown method.
 """
 from __future__ import annotations
 
@@ -30,7 +31,7 @@ import numpy as np
 
 RUN_RECORD_HEADER = ("problem,method,nu,grid_size,rmse,runtime_seconds,iterations,sigma_hat,converged,"
                      "combine_invocations,sequential_depth")
-METHODS = ("paraieks", "paraieks-elements")
+METHODS = ("paraieks", "paraieks-elements", "eks")
 PROBLEMS = ("logistic", "rigidbody", "vanderpol")
 
 
@@ -97,6 +98,8 @@ def _solver(method: str):
     import paraode_b200 as P
 
     def run(prob, prior, grid, config):
+        if method == "eks":  # bench.cpp:139
+            return P.eks_solve(prob, prior, grid, config.linearization)
         if method == "paraieks-elements":
             old = os.environ.get("PODE_IEKS_ENGINE")
             os.environ["PODE_IEKS_ENGINE"] = "elements"

@@ -557,14 +557,17 @@ int pode_rts(pode_context* ctx, const pode_chain* chain, pode_rts_out out, pode_
   });
 }
 
-int pode_ieks(pode_context* ctx, const pode_problem* problem, const pode_prior* prior, const double* grid,
-              int64_t n_nodes, const pode_ieks_config* config, pode_ieks_report* report, pode_status* status) {
+// pode_ieks and pode_eks: argument checks, output staging and the report.
+static int solve_report(pode_context* ctx, const pode_problem* problem, const pode_prior* prior, const double* grid,
+                        int64_t n_nodes, const pode_ieks_config* config, pode_ieks_report* report,
+                        pode_status* status, bool eks) {
   return guarded(status, [&] {
     check_ctx(ctx);
     if (problem == nullptr || prior == nullptr || grid == nullptr || config == nullptr || report == nullptr)
-      throw ApiError(PODE_ERR_INVALID_INPUT, "ieks: NULL argument");
+      throw ApiError(PODE_ERR_INVALID_INPUT, eks ? "eks_solve: NULL argument" : "ieks: NULL argument");
     const host::Problem p = host::resolve_problem(*problem);
-    if (p.dim != prior->dim) throw ApiError(PODE_ERR_DIMENSION, "ieks: problem and prior dimensions disagree");
+    if (p.dim != prior->dim)
+      throw ApiError(PODE_ERR_DIMENSION, std::string(eks ? "eks_solve" : "ieks") + ": problem and prior dimensions disagree");
     if (config->max_iterations < 1) throw ApiError(PODE_ERR_INVALID_INPUT, "ieks: max_iterations must be at least 1");
     if (prior->nu < 1 || prior->dim < 1) throw ApiError(PODE_ERR_INVALID_INPUT, "IwpPrior: need nu >= 1 and dim >= 1");
     if (!(prior->sigma >= 0.0) || !std::isfinite(prior->sigma))
@@ -584,7 +587,7 @@ int pode_ieks(pode_context* ctx, const pode_problem* problem, const pode_prior* 
     double* sc = dev ? report->solution_covs
                      : (report->solution_covs ? ctx->ws.arr<double>("out_sc", n_nodes * d * d) : nullptr);
     IeksResult r;
-    ops.ieks(ctx, p, *prior, grid, n_nodes, *config, means, cov, sm, sc, &r);
+    (eks ? ops.eks : ops.ieks)(ctx, p, *prior, grid, n_nodes, *config, means, cov, sm, sc, &r);
     if (!dev) {
       stage_out(ctx, report->means, means, size_t(n_nodes) * D, false);
       stage_out(ctx, report->cov_sqrt, cov, size_t(n_nodes) * D * D, false);
@@ -600,6 +603,17 @@ int pode_ieks(pode_context* ctx, const pode_problem* problem, const pode_prior* 
       for (int k = 0; k < int(r.trace.size()) && k < report->trace_capacity; ++k)
         report->objective_trace[k] = r.trace[k];
   });
+}
+
+int pode_ieks(pode_context* ctx, const pode_problem* problem, const pode_prior* prior, const double* grid,
+              int64_t n_nodes, const pode_ieks_config* config, pode_ieks_report* report, pode_status* status) {
+  return solve_report(ctx, problem, prior, grid, n_nodes, config, report, status, false);
+}
+
+int pode_eks(pode_context* ctx, const pode_problem* problem, const pode_prior* prior, const double* grid,
+             int64_t n_nodes, int32_t linearization, pode_ieks_report* report, pode_status* status) {
+  const pode_ieks_config cfg{1, 0.0, 0.0, 0.0, linearization};
+  return solve_report(ctx, problem, prior, grid, n_nodes, &cfg, report, status, true);
 }
 
 int pode_rk4_table(pode_context* ctx, const pode_problem* problem, int64_t steps, double* table,

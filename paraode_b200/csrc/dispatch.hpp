@@ -29,6 +29,9 @@ struct EngineOps {
   void (*ieks_sharded)(pode_context*, const host::Problem&, const pode_prior&, const double*, int64_t,
                        const pode_ieks_config&, const pode_shard_comm&, double*, double*, double*, double*,
                        IeksResult*);
+  // eks_solve (element engine; cfg.linearization only)
+  void (*eks)(pode_context*, const host::Problem&, const pode_prior&, const double*, int64_t,
+              const pode_ieks_config&, double*, double*, double*, double*, IeksResult*);
 };
 
 // Shard s of R owns steps [floor(N s / R), floor(N (s+1) / R)).

@@ -303,6 +303,66 @@ struct IeksSetup {
   DevProblem prob{};
 };
 
+// eks_solve's forward pass (ieks.cpp:237-250): group 0 of one warp walks the
+// N steps in order, linearising step n at its own predicted mean
+// eta = T_{n+1} ⊙ m^- (k_linearize's formulas, statespace.cpp:65-103); the
+// step's observation model lands in the chain (H, offset), the filtered
+// marginals in fm / fc (rescaled coordinates).  Inherently sequential: the
+// linearisation point of step n depends on the filter up to step n.
+template <int D>
+__global__ void __launch_bounds__(32) k_eks_forward(DevChain ch, DevProblem prob, int nu, const double* scale,
+                                                    int ek0, double* fm, double* fc, DevError* err) {
+  extern __shared__ double smem[];
+  const Grp<D> g = make_group<D>(smem);
+  const bool ok = g.real() && g.gw == 0;
+  const int d = prob.dim, b = nu + 1;
+  double* const h = const_cast<double*>(ch.h);
+  double* const off = const_cast<double*>(ch.off);
+  Gauss<D> f;
+  f.m = ok ? ch.init_mean[g.r] : 0.0;
+  f.c = ld_row<D>(ch.init_cov, 0, g.r, ok);
+  st_ent<D>(fm, 0, g.r, ok, f.m);
+  st_row<D>(fc, 0, g.r, ok, f.c);
+#pragma unroll 1
+  for (int64_t n = 0; n < ch.N; ++n) {
+    const Rw<D> phi = chain_phi<D>(ch, n, g.r, ok);
+    const Rw<D> q = chain_q<D>(ch, n, g.r, ok);
+    Gauss<D> p = kf_predict(g, f, phi, q);
+    const double* s = scale + (n + 1) * D;
+    const Rw<D> eta = gather_vec(g, ok ? s[g.r] * p.m : 0.0);
+    if (ok && g.r < d) {
+      double y[D], fv[D], jac[D * D];
+      for (int r = 0; r < d; ++r) y[r] = eta[r * b];
+      eval_field<D>(prob, y, fv, jac);
+      const int r = g.r;
+      bool finite = isfinite(fv[r]);
+      if (!ek0)
+        for (int c = 0; c < d; ++c) finite &= isfinite(jac[r * D + c]);
+      if (!finite) raise_error(err, n + 1, kErrLinearization);
+      double* hr = h + (n * d + r) * D;
+      for (int c = 0; c < D; ++c) hr[c] = 0.0;
+      hr[r * b + 1] = 1.0 * s[r * b + 1];
+      if (ek0) {
+        off[n * d + r] = fv[r];
+      } else {
+        double jy = 0.0;
+        for (int c = 0; c < d; ++c) {
+          hr[c * b] = -jac[r * D + c] * s[c * b];
+          jy += jac[r * D + c] * y[c];
+        }
+        off[n * d + r] = fv[r] - jy;
+      }
+    }
+    wsync();  // the step's H rows and offsets, written by lanes 0..d-1, are read by the whole group
+    const Obs<D, D> o = load_obs<D>(ch, n, g.r, ok);
+    const bool good = kf_update<D, D>(g, p, o);
+    if (ok && g.r == 0 && !good) raise_error(err, n + 1, kErrSingular);
+    f = p;
+    st_ent<D>(fm, n + 1, g.r, ok, f.m);
+    st_row<D>(fc, n + 1, g.r, ok, f.c);
+  }
+}
+
 template <int D>
 struct IeksEngine {
   // node_scales = false (fused engine): T_n is recomputed in the kernels, so
@@ -402,20 +462,97 @@ struct IeksEngine {
   }
 
   // node_offset: global index of local node 0 (time-axis shards).
-  static void check_linearization(pode_context* ctx, const IeksSetup<D>& s, int it, int64_t node_offset = 0) {
+  // `what` (default "ieks iteration <it>") prefixes the message.
+  static void check_linearization(pode_context* ctx, const IeksSetup<D>& s, int it, int64_t node_offset = 0,
+                                  const char* what = nullptr) {
     const unsigned long long key = fetch_error(ctx);
     if (key == ~0ull) return;
     const int code = int(key & 0xff);
     const int64_t idx = int64_t(key >> 8) + node_offset;
+    const std::string pre = what ? std::string(what) : "ieks iteration " + std::to_string(it);
     if (code == kErrLinearization) {
       double t = 0.0;
       cuda_check(cudaMemcpy(&t, s.grid + idx, sizeof(double), cudaMemcpyDeviceToHost), "t");
-      throw ApiError(PODE_ERR_LINEARIZATION,
-                     "ieks iteration " + std::to_string(it) + ": linearize: vector field evaluation is not finite",
-                     idx, t, it);
+      throw ApiError(PODE_ERR_LINEARIZATION, pre + ": linearize: vector field evaluation is not finite", idx, t, it);
     }
-    throw ApiError(PODE_ERR_SINGULAR_FACTOR,
-                   "ieks iteration " + std::to_string(it) + ": smoother: triangular factor is singular", idx, 0.0, it);
+    throw ApiError(PODE_ERR_SINGULAR_FACTOR, pre + (what ? ": filter" : ": smoother") + ": triangular factor is singular",
+                   idx, 0.0, it);
+  }
+
+  // eks_solve (ieks.cpp:224-291): the sequential forward pass linearised at
+  // the predicted means (k_eks_forward), the smoother of those filtered
+  // marginals as the reverse ⊗_s scan, calibration, the objective of the
+  // smoothed means and the outputs.  One "iteration", converged.
+  static IeksResult run_eks(pode_context* ctx, const host::Problem& p, const pode_prior& prior, const double* grid_h,
+                            int64_t n1, const pode_ieks_config& cfg, double* means, double* cov, double* sol_m,
+                            double* sol_c) {
+    IeksSetup<D> s;
+    setup(ctx, p, prior, grid_h, n1, s);
+    cudaStream_t st = ctx->stream;
+    Workspace& ws = ctx->ws;
+    DevError* err = reinterpret_cast<DevError*>(ctx->d_err);
+    const int64_t N = s.N;
+    const DevChain ch = chain(ctx, s, true);
+    double* fm = ws.arr<double>("ieks_fm", n1 * D);
+    double* fc = ws.arr<double>("ieks_fc", n1 * D * D);
+    double* sm = ws.arr<double>("ieks_sm", n1 * D);
+    double* sc = ws.arr<double>("ieks_sc", n1 * D * D);
+    const int fwd_smem = int(sizeof(double) * Grp<D>::kSlots * Scratch<D>::kDoubles);
+    cuda_check(cudaFuncSetAttribute(k_eks_forward<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem),
+               "eks smem");
+    reset_error(ctx);
+    k_eks_forward<D><<<1, 32, fwd_smem, st>>>(ch, s.prob, s.nu, s.scale, cfg.linearization, fm, fc, err);
+    note_launch(ctx, "eks_forward");
+    check_linearization(ctx, s, 1, 0, "eks_solve");
+    // rts_smooth_pass of the sequential filter (sequential.cpp:105-132) as the reverse scan
+    SEd se = Engine<D>::template alloc<SOps<D>>(ctx, "rts_se", N + 1);
+    Engine<D>::make_smoothing(ctx, ch, fm, fc, se);
+    const ScanTally t = Engine<D>::scan_smoothing(ctx, N + 1, se, se, true);
+    cuda_check(cudaMemcpyAsync(sm, se.g, sizeof(double) * D * n1, cudaMemcpyDeviceToDevice, st), "smoothed");
+    cuda_check(cudaMemcpyAsync(sc, se.l, sizeof(double) * D * D * n1, cudaMemcpyDeviceToDevice, st), "smoothed");
+    IeksResult res;
+    res.stats.combines = t.combines;
+    res.stats.depth = t.depth;
+    // innovation statistics and calibration (ieks.cpp:79-109)
+    double* vals = ws.arr<double>("ieks_innov", N);
+    cuda_check(cudaFuncSetAttribute(k_innovation<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(smem_bytes<D>())),
+               "innovation smem");
+    k_innovation<D><<<blocks_for<D>(N), kThreads, smem_bytes<D>(), st>>>(ch, fm, fc, vals, err);
+    note_launch(ctx, "innovation");
+    const int64_t np2 = grid1(N);
+    double* part2 = ws.arr<double>("ieks_part2", np2 * 3 + 3);
+    k_sum_blocks<<<np2, kRedThreads, 0, st>>>(vals, N, part2);
+    note_launch(ctx, "sum_blocks");
+    k_finish3<<<1, kRedThreads, 0, st>>>(part2, np2, part2 + np2 * 3);
+    note_launch(ctx, "finish3");
+    cuda_check(cudaMemcpyAsync(ctx->h_scalars, part2 + np2 * 3, sizeof(double), cudaMemcpyDeviceToHost, st),
+               "innov");
+    check_linearization(ctx, s, 1, 0, "eks_solve");  // syncs
+    const double sigma_rel = std::sqrt(ctx->h_scalars[0] / double(N * s.dim));
+    res.sigma_hat = sigma_rel * prior.sigma;
+    // original-coordinate means and the objective of the smoothed trajectory (ieks.cpp:279-289)
+    double* eta_old = ws.arr<double>("ieks_eta_a", n1 * D);
+    double* eta_out = ws.arr<double>("ieks_eta_b", n1 * D);
+    k_fill_rows<<<grid1(n1 * D), kRedThreads, 0, st>>>(s.mu0, n1, D, eta_old);
+    note_launch(ctx, "fill");
+    const int64_t nparts = grid1(n1);
+    double* part = ws.arr<double>("ieks_part", nparts * 3 + 3);
+    k_eta_objective<<<grid1(n1), kRedThreads, 0, st>>>(sm, s.scale, s.scale_inv, eta_old, ch.phi, s.qunit, s.qinv,
+                                                       n1, D, eta_out, part);
+    note_launch(ctx, "eta_objective");
+    k_finish3<<<1, kRedThreads, 0, st>>>(part, nparts, part + nparts * 3);
+    note_launch(ctx, "finish3");
+    cuda_check(cudaMemcpyAsync(ctx->h_scalars, part + nparts * 3, sizeof(double) * 3, cudaMemcpyDeviceToHost, st),
+               "objective");
+    k_outputs<<<grid1(n1), kRedThreads, 0, st>>>(eta_out, sc, s.scale, sigma_rel, n1, D, s.nu, s.dim, means, cov,
+                                                 sol_m, sol_c);
+    note_launch(ctx, "outputs");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    res.trace.push_back(0.5 * ctx->h_scalars[0]);
+    res.iterations = 1;
+    res.converged = true;
+    return res;
   }
 
   // After the loop: smoothing covariances and the filtered marginals of the

@@ -102,7 +102,11 @@ void iks(pode_context* c, const host::Problem& p, const pode_prior& pr, const do
   }
   throw ApiError(PODE_ERR_UNSUPPORTED, "ieks_sharded: needs an ODE operator the fused engine serves (d <= 3, D <= 9)");
 }
-const EngineOps kOps{kD, cf, cs, mf, ms, sf, ss, rt, ik, iks};
+void ek(pode_context* c, const host::Problem& p, const pode_prior& pr, const double* g, int64_t n1,
+        const pode_ieks_config& cfg, double* m, double* cv, double* sm, double* sc, IeksResult* out) {
+  *out = IeksEngine<kD>::run_eks(c, p, pr, g, n1, cfg, m, cv, sm, sc);
+}
+const EngineOps kOps{kD, cf, cs, mf, ms, sf, ss, rt, ik, iks, ek};
 }  // namespace
 
 const EngineOps* PODE_CAT(engine_ops_d, PODE_D)() { return &kOps; }

@@ -10,11 +10,11 @@ from paraode_b200 import cli
 
 
 def test_methods_and_unknowns():  # test_cli.cpp:40-45
-    assert cli.METHODS == ("paraieks", "paraieks-elements")
+    assert cli.METHODS == ("paraieks", "paraieks-elements", "eks")
     with pytest.raises(cli.UsageError):
         cli._solver("rk45")
-    with pytest.raises(cli.UsageError):  # the reference's sequential CPU baselines are not on this path
-        cli._solver("eks")
+    with pytest.raises(cli.UsageError):  # the reference's sequential CPU baseline is not on this path
+        cli._solver("ieks")
 
 
 def test_csv_schema_is_stable():  # test_cli.cpp:47-72
@@ -43,6 +43,16 @@ def test_chart_tolerates_empty_and_partial_input():  # test_cli.cpp:74-93
                                   ["benchmark", "--repeats", "0"], ["solve", "--method", "rk45"]])
 def test_solve_rejects_unusable_arguments(argv):  # test_cli.cpp:128-134
     assert cli.main(argv) == 1
+
+
+@pytest.mark.gpu
+def test_solve_eks_method(tmp_path):  # bench.cpp:139 (Method::kEks): one pass, converged, exit 0
+    out = tmp_path / "eks.json"
+    assert cli.main(["solve", "--problem", "logistic", "--method", "eks", "--n", "30", "--nu", "2",
+                     "--out", str(out)]) == 0
+    doc = json.loads(out.read_text())
+    assert doc["method"] == "eks" and doc["iterations"] == 1 and doc["converged"] is True
+    assert len(doc["objective_trace"]) == 1 and math.isclose(doc["mean"][30][0], 0.9955, rel_tol=1e-2)
 
 
 @pytest.mark.gpu

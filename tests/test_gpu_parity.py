@@ -373,3 +373,40 @@ def test_full_size_fhn_properties():
     assert err <= 1e-9  # measured 1.0e-11
     var = np.diagonal(a.solution_covs, axis1=1, axis2=2)
     assert np.all(np.isfinite(a.cov_sqrt)) and np.all(var[1:] > 0.0)
+
+
+# -------------------------------------------------------------- eks ---
+EKS_CASES = [("logistic", 1, 30, False), ("logistic", 2, 64, True), ("vanderpol", 2, 100, False),
+             ("rigidbody", 2, 150, False), ("fhn", 2, 256, False), ("vanderpol", 3, 200, True),
+             ("rigidbody", 4, 300, False), ("logistic", 1, 1024, False)]
+
+
+@pytest.mark.parametrize("name,nu,steps,ek0", EKS_CASES)
+def test_eks_solve_matches_oracle(name, nu, steps, ek0):  # eks_solve, ieks.cpp:224-291 (bench.cpp:139)
+    op = O.problem(name)
+    grid = O.uniform_grid(op.t_end, steps)
+    want = O.ieks(op, nu, grid, mode=-1, ek0=ek0)
+    got = P.eks_solve(P.problem_by_name(name), P.IwpPrior(nu, op.dim, 1.0), grid, "ek0" if ek0 else "ek1")
+    assert got.iterations == want["iterations"] == 1 and got.converged and want["converged"]
+    assert rel(got.means, want["means"]) <= 1e-9
+    assert rel(dense_cov(got.cov_sqrt), dense_cov(want["cov_sqrt"])) <= 1e-7
+    assert got.sigma_hat == pytest.approx(want["sigma_hat"], rel=1e-7)
+    assert rel(got.solution_means, want["solution_means"]) <= 1e-9
+    assert rel(got.solution_covs, want["solution_covs"]) <= 1e-7
+    assert np.allclose(got.objective_trace, want["objective_trace"], rtol=1e-8, atol=1e-12)
+
+
+def test_eks_ragged_grid_and_errors():
+    g = np.cumsum(np.concatenate([[0.0], 0.05 + 0.1 * np.abs(np.sin(np.arange(80)))]))
+    got = P.eks_solve(P.van_der_pol(), P.IwpPrior(2, 2, 1.0), g)
+    want = O.ieks(O.problem("vanderpol"), 2, g, mode=-1)
+    assert rel(got.means, want["means"]) <= 1e-9
+    assert rel(dense_cov(got.cov_sqrt), dense_cov(want["cov_sqrt"])) <= 1e-7
+    with pytest.raises(P.DimensionError):
+        P.eks_solve(P.van_der_pol(), P.IwpPrior(2, 3, 1.0), g)
+    with pytest.raises(P.InvalidInputError):
+        P.eks_solve(P.van_der_pol(), P.IwpPrior(2, 2, 1.0), [0.5, 1.0])
+    # deterministic run to run
+    again = P.eks_solve(P.van_der_pol(), P.IwpPrior(2, 2, 1.0), g)
+    assert np.array_equal(again.means, got.means) and np.array_equal(again.cov_sqrt, got.cov_sqrt)
+
