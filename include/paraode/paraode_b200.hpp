@@ -225,6 +225,14 @@ struct SolverReport {  // ieks.hpp:77-87
   ScanStats scan_stats;
 };
 
+namespace detail {
+template <class Matrix, class Vector>
+SolverReport<Matrix, Vector> report(const std::vector<double>& grid, int D, int d, const std::vector<double>& means,
+                                    const std::vector<double>& cov, const std::vector<double>& sm,
+                                    const std::vector<double>& sc, const std::vector<double>& trace,
+                                    const pode_ieks_report& rep);
+}  // namespace detail
+
 // para_ieks (ieks.hpp:95-96).
 template <class Matrix, class Vector>
 SolverReport<Matrix, Vector> para_ieks(const Problem& problem, const IwpPrior& prior,
@@ -242,6 +250,16 @@ SolverReport<Matrix, Vector> para_ieks(const Problem& problem, const IwpPrior& p
                        PODE_HOST, 0, 0, 0.0, {0, 0}};
   pode_status st{};
   check(pode_ieks(dev.handle(), &p, &pr, grid.data(), n1, &cfg, &rep, &st), st);
+  return detail::report<Matrix, Vector>(grid, D, d, means, cov, sm, sc, trace, rep);
+}
+
+namespace detail {
+template <class Matrix, class Vector>
+SolverReport<Matrix, Vector> report(const std::vector<double>& grid, int D, int d, const std::vector<double>& means,
+                                    const std::vector<double>& cov, const std::vector<double>& sm,
+                                    const std::vector<double>& sc, const std::vector<double>& trace,
+                                    const pode_ieks_report& rep) {
+  const int64_t n1 = int64_t(grid.size());
   SolverReport<Matrix, Vector> out;
   out.times = grid;
   out.marginals.resize(size_t(n1));
@@ -260,6 +278,25 @@ SolverReport<Matrix, Vector> para_ieks(const Problem& problem, const IwpPrior& p
   out.scan_stats.combine_invocations = std::size_t(rep.scan_stats.combine_invocations);
   out.scan_stats.sequential_depth = std::size_t(rep.scan_stats.sequential_depth);
   return out;
+}
+}  // namespace detail
+
+// eks_solve (ieks.hpp:103-105): one pass linearised at the predicted means.
+template <class Matrix, class Vector>
+SolverReport<Matrix, Vector> eks_solve(const Problem& problem, const IwpPrior& prior, const std::vector<double>& grid,
+                                       Linearization linearization, Device& dev) {
+  const int D = prior.state_dim(), d = prior.dim;
+  const int64_t n1 = int64_t(grid.size());
+  pode_problem p{int32_t(problem.kind), problem.dim, problem.t_end, problem.y0.data(),
+                 problem.params.empty() ? nullptr : problem.params.data(), int32_t(problem.params.size())};
+  pode_prior pr{prior.nu, prior.dim, prior.sigma};
+  std::vector<double> means(size_t(n1) * D), cov(size_t(n1) * D * D), sm(size_t(n1) * d), sc(size_t(n1) * d * d);
+  std::vector<double> trace(1);
+  pode_ieks_report rep{means.data(), cov.data(), sm.data(), sc.data(), trace.data(), 1, PODE_HOST, 0, 0, 0.0, {0, 0}};
+  pode_status st{};
+  check(pode_eks(dev.handle(), &p, &pr, grid.data(), n1, linearization == Linearization::kEk0 ? 1 : 0, &rep, &st),
+        st);
+  return detail::report<Matrix, Vector>(grid, D, d, means, cov, sm, sc, trace, rep);
 }
 
 // para_ieks over time-axis shard `rank` of `ranks` (one process per GPU;

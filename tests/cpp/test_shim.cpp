@@ -61,6 +61,10 @@ int main() {
     for (int n = 0; n <= 30; ++n) grid[n] = 10.0 * n / 30.0;
     auto rep = pb::para_ieks<Mat, Vec>(p, pb::IwpPrior{2, 1, 1.0}, grid, pb::IeksConfig{}, gpu);
     CHECK(rep.converged);
+    // eks_solve (ieks.hpp:103-105): one pass, converged, close to the IEKS posterior here
+    auto eks = pb::eks_solve<Mat, Vec>(p, pb::IwpPrior{2, 1, 1.0}, grid, pb::Linearization::kEk1, gpu);
+    CHECK(eks.converged && eks.iterations == 1 && eks.objective_trace.size() == 1);
+    CHECK(std::fabs(eks.solution_means.back()[0] - rep.solution_means.back()[0]) <= 1e-2);
     const double want = 0.01 / (0.01 + 0.99 * std::exp(-10.0));
     std::printf("logistic: iterations %d, y(10) = %.12f (want %.12f), sigma_hat %.6g\n", rep.iterations,
                 rep.solution_means.back()[0], want, rep.sigma_hat);
