@@ -410,3 +410,19 @@ def test_eks_ragged_grid_and_errors():
     again = P.eks_solve(P.van_der_pol(), P.IwpPrior(2, 2, 1.0), g)
     assert np.array_equal(again.means, got.means) and np.array_equal(again.cov_sqrt, got.cov_sqrt)
 
+
+
+@pytest.mark.parametrize("n", [40, 100_000])  # serial and OpenMP-split grid checks
+def test_non_increasing_grid_rejected(n):  # discretize, ieks.cpp:8-20
+    prior = P.IwpPrior(2, 2, 1.0)
+    for k in (1, n // 2, n - 1):
+        g = O.uniform_grid(6.3, n)
+        g[k + 1] = g[k]
+        with pytest.raises(P.InvalidInputError, match="strictly increasing"):
+            P.para_ieks(P.van_der_pol(), prior, g)
+        with pytest.raises(P.InvalidInputError, match="strictly increasing"):
+            P.eks_solve(P.van_der_pol(), prior, g)
+    g = O.uniform_grid(6.3, n)
+    g[n // 3] = np.nan
+    with pytest.raises(P.InvalidInputError):
+        P.para_ieks(P.van_der_pol(), prior, g)
