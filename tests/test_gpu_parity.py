@@ -259,6 +259,23 @@ def test_fused_engine_variants(monkeypatch, env):
     assert got.sigma_hat == pytest.approx(want["sigma_hat"], rel=1e-7)
 
 
+@pytest.mark.parametrize("name,steps", [("fhn", 720), ("fhn", 1200), ("fhn", 1800), ("rigidbody", 600),
+                                        ("fhn", 2400)])
+def test_block_scan_tiles(monkeypatch, name, steps):
+    """Block-scan levels of 2..5 blocks (G = 40 at D = 6, 24 at D = 9) at
+    every level above 0, and the down-sweeps that apply their carries."""
+    monkeypatch.setenv("PODE_CHUNK", "3")
+    monkeypatch.setenv("PODE_SCAN_FANIN", "4")
+    monkeypatch.setenv("PODE_BSCAN", "1")
+    op = O.problem(name)
+    grid = O.uniform_grid(op.t_end, steps)
+    want = O.ieks(op, 2, grid, mode=0)
+    got = P.para_ieks(P.problem_by_name(name), P.IwpPrior(2, op.dim, 1.0), grid)
+    assert got.iterations == want["iterations"]
+    assert rel(got.means, want["means"]) <= 1e-9
+    assert rel(dense_cov(got.cov_sqrt), dense_cov(want["cov_sqrt"])) <= 1e-7
+
+
 def test_logistic_frozen_rmse():  # acceptance.cpp:167-179 — reference measured 1.374e-6, gate 2.1e-6
     from _dense import logistic_reference, rmse
     grid = O.uniform_grid(10.0, 30)
