@@ -323,13 +323,26 @@ __global__ void __launch_bounds__(32) k_eks_forward(DevChain ch, DevProblem prob
   f.c = ld_row<D>(ch.init_cov, 0, g.r, ok);
   st_ent<D>(fm, 0, g.r, ok, f.m);
   st_row<D>(fc, 0, g.r, ok, f.c);
+  // phi_n is loaded one step ahead; the step's observation rows are built
+  // in registers (lane r < d owns row r; R = 0, padded rows carry the unit
+  // dummy of load_obs) and only written out for the smoother / innovations
+  Rw<D> phi_next = chain_phi<D>(ch, 0, g.r, ok);
 #pragma unroll 1
   for (int64_t n = 0; n < ch.N; ++n) {
-    const Rw<D> phi = chain_phi<D>(ch, n, g.r, ok);
+    const Rw<D> phi = phi_next;
+    phi_next = chain_phi<D>(ch, n + 1 < ch.N ? n + 1 : n, g.r, ok);
     const Rw<D> q = chain_q<D>(ch, n, g.r, ok);
     Gauss<D> p = kf_predict(g, f, phi, q);
     const double* s = scale + (n + 1) * D;
     const Rw<D> eta = gather_vec(g, ok ? s[g.r] * p.m : 0.0);
+    Obs<D, D> o;
+    o.m = ok ? d : 0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      o.h[j] = 0.0;
+      o.r[j] = ((!ok || g.r >= d) && j == g.r) ? 1.0 : 0.0;
+    }
+    o.off = 0.0;
     if (ok && g.r < d) {
       double y[D], fv[D], jac[D * D];
       for (int r = 0; r < d; ++r) y[r] = eta[r * b];
@@ -339,22 +352,27 @@ __global__ void __launch_bounds__(32) k_eks_forward(DevChain ch, DevProblem prob
       if (!ek0)
         for (int c = 0; c < d; ++c) finite &= isfinite(jac[r * D + c]);
       if (!finite) raise_error(err, n + 1, kErrLinearization);
-      double* hr = h + (n * d + r) * D;
-      for (int c = 0; c < D; ++c) hr[c] = 0.0;
-      hr[r * b + 1] = 1.0 * s[r * b + 1];
+      double ov;
       if (ek0) {
-        off[n * d + r] = fv[r];
+        ov = fv[r];
       } else {
         double jy = 0.0;
-        for (int c = 0; c < d; ++c) {
-          hr[c * b] = -jac[r * D + c] * s[c * b];
-          jy += jac[r * D + c] * y[c];
-        }
-        off[n * d + r] = fv[r] - jy;
+        for (int c = 0; c < d; ++c) jy += jac[r * D + c] * y[c];
+        ov = fv[r] - jy;
       }
+#pragma unroll
+      for (int j = 0; j < D; ++j) {  // H = E_1 - F_y E_0, rescaled (k_linearize)
+        double v = 0.0;
+        if (j == r * b + 1)
+          v = 1.0 * s[j];
+        else if (!ek0 && j % b == 0)
+          v = -jac[r * D + j / b] * s[j];
+        o.h[j] = v;
+        h[(n * d + r) * D + j] = v;
+      }
+      o.off = ov;
+      off[n * d + r] = ov;
     }
-    wsync();  // the step's H rows and offsets, written by lanes 0..d-1, are read by the whole group
-    const Obs<D, D> o = load_obs<D>(ch, n, g.r, ok);
     const bool good = kf_update<D, D>(g, p, o);
     if (ok && g.r == 0 && !good) raise_error(err, n + 1, kErrSingular);
     f = p;
