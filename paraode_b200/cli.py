@@ -13,9 +13,9 @@
   (bench.cpp:290-318); exit 0 all pass, 1 otherwise.
 
 Methods: `paraieks` (the fused engine), `paraieks-elements` (element
-engine) and `eks` (the non-iterated smoother, eks_solve, on the device).
-The reference's sequential CPU `ieks` baseline is not part of the B200 path
-and is rejected as an unknown method.
+engine), `ieks` (seq_ieks: the same iterates with the whole grid in one
+chunk, i.e. the Kalman folds run in time order in one thread; fused-engine
+states, D <= 9) and `eks` (the non-iterated smoother, eks_solve).
 """
 from __future__ import annotations
 
@@ -31,7 +31,7 @@ import numpy as np
 
 RUN_RECORD_HEADER = ("problem,method,nu,grid_size,rmse,runtime_seconds,iterations,sigma_hat,converged,"
                      "combine_invocations,sequential_depth")
-METHODS = ("paraieks", "paraieks-elements", "eks")
+METHODS = ("paraieks", "paraieks-elements", "ieks", "eks")
 PROBLEMS = ("logistic", "rigidbody", "vanderpol")
 
 
@@ -97,19 +97,27 @@ def _solver(method: str):
         raise UsageError(f"unknown method '{method}' (expected {', '.join(METHODS)})")
     import paraode_b200 as P
 
+    def with_env(key, value, fn):
+        old = os.environ.get(key)
+        os.environ[key] = value
+        try:
+            return fn()
+        finally:
+            if old is None:
+                del os.environ[key]
+            else:
+                os.environ[key] = old
+
     def run(prob, prior, grid, config):
         if method == "eks":  # bench.cpp:139
             return P.eks_solve(prob, prior, grid, config.linearization)
+        if method == "ieks":  # bench.cpp:138: seq_ieks = the same iterates, time-sequential
+            # one chunk: a single lane thread runs every Kalman fold in time
+            # order (fused engine, D <= 9; larger states use the element engine)
+            return with_env("PODE_CHUNK", str(max(2, len(grid) - 1)),
+                            lambda: P.para_ieks(prob, prior, grid, config))
         if method == "paraieks-elements":
-            old = os.environ.get("PODE_IEKS_ENGINE")
-            os.environ["PODE_IEKS_ENGINE"] = "elements"
-            try:
-                return P.para_ieks(prob, prior, grid, config)
-            finally:
-                if old is None:
-                    del os.environ["PODE_IEKS_ENGINE"]
-                else:
-                    os.environ["PODE_IEKS_ENGINE"] = old
+            return with_env("PODE_IEKS_ENGINE", "elements", lambda: P.para_ieks(prob, prior, grid, config))
         return P.para_ieks(prob, prior, grid, config)
     return run
 

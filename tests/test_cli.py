@@ -4,17 +4,18 @@ errors and exit codes on CPU; solve / benchmark / compare on the GPU."""
 import json
 import math
 
+import numpy as np
 import pytest
 
 from paraode_b200 import cli
 
 
 def test_methods_and_unknowns():  # test_cli.cpp:40-45
-    assert cli.METHODS == ("paraieks", "paraieks-elements", "eks")
+    assert cli.METHODS == ("paraieks", "paraieks-elements", "ieks", "eks")
     with pytest.raises(cli.UsageError):
         cli._solver("rk45")
-    with pytest.raises(cli.UsageError):  # the reference's sequential CPU baseline is not on this path
-        cli._solver("ieks")
+    with pytest.raises(cli.UsageError):
+        cli._solver("seq")
 
 
 def test_csv_schema_is_stable():  # test_cli.cpp:47-72
@@ -53,6 +54,22 @@ def test_solve_eks_method(tmp_path):  # bench.cpp:139 (Method::kEks): one pass, 
     doc = json.loads(out.read_text())
     assert doc["method"] == "eks" and doc["iterations"] == 1 and doc["converged"] is True
     assert len(doc["objective_trace"]) == 1 and math.isclose(doc["mean"][30][0], 0.9955, rel_tol=1e-2)
+
+
+@pytest.mark.gpu
+def test_ieks_method_matches_paraieks():  # acceptance.cpp:97-123: seq and par agree, equal iterations
+    import paraode_b200 as P
+    import _oracle as O
+    for name, nu, n in (("logistic", 2, 60), ("vanderpol", 2, 200), ("fhn", 2, 300)):
+        prob = P.problem_by_name(name)
+        prior = P.IwpPrior(nu, prob.dim, 1.0)
+        grid = P.uniform_grid(prob.t_end, n)
+        seq = cli._solver("ieks")(prob, prior, grid, P.IeksConfig())
+        par = cli._solver("paraieks")(prob, prior, grid, P.IeksConfig())
+        want = O.ieks(O.problem(name), nu, grid, mode=0)
+        assert seq.iterations == par.iterations == want["iterations"]
+        assert np.max(np.abs(seq.means - par.means)) <= 1e-8 * max(1.0, np.max(np.abs(par.means)))
+        assert np.max(np.abs(seq.means - want["means"])) <= 1e-9 * max(1.0, np.max(np.abs(want["means"])))
 
 
 @pytest.mark.gpu
