@@ -176,7 +176,9 @@ typedef enum {
   PODE_VAN_DER_POL = 3,/* params[0] = mu                       (problems.cpp:159-179) */
   PODE_FITZHUGH_NAGUMO = 4, /* params = (a, b, c)              (new) */
   PODE_PLEIADES = 5,   /* 7-body, first order, d = 28          (new) */
-  PODE_AFFINE = 6      /* y' = L y + c; params = L (d*d row-major), c (d) */
+  PODE_AFFINE = 6,     /* y' = L y + c; params = L (d*d row-major), c (d) */
+  PODE_POLE = 7        /* y' = 1 / (t - a), d = 1, params = {a}: the reference's non-finite
+                          field test (test_statespace.cpp:123-139) with the pole at time a */
 } pode_problem_kind;
 
 typedef struct {

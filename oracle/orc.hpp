@@ -164,6 +164,7 @@ enum ProblemKind : int {
   kFitzHughNagumo = 4,
   kPleiades = 5,
   kAffine = 6,
+  kPole = 7,  // test kind: y' = 1 / (t - a), the reference's non-finite-field case
 };
 struct Problem {
   int kind = 0;

@@ -91,7 +91,7 @@ namespace {
 constexpr int kBodies = 7;
 
 template <typename S>
-std::vector<S> eval_field(const Problem& p, const std::vector<S>& y) {
+std::vector<S> eval_field(const Problem& p, const std::vector<S>& y, const S& t) {
   std::vector<S> out(static_cast<std::size_t>(p.dim), y[0]);
   switch (p.kind) {
     case kLogistic:  // problems.cpp:83-88
@@ -150,6 +150,11 @@ std::vector<S> eval_field(const Problem& p, const std::vector<S>& y) {
       }
       break;
     }
+    case kPole: {  // the reference's non-finite-field test (test_statespace.cpp:123-139), as a
+                   // time pole so the failing node is known: y' = 1 / (t - a)
+      out[0] = (y[0] * 0.0 + 1.0) / (t - p.params[0]);
+      break;
+    }
     default:
       throw InvalidInputError("unknown problem kind");
   }
@@ -158,10 +163,10 @@ std::vector<S> eval_field(const Problem& p, const std::vector<S>& y) {
 
 }  // namespace
 
-Vec field(const Problem& p, const Vec& y, double) { return eval_field<double>(p, y); }
+Vec field(const Problem& p, const Vec& y, double t) { return eval_field<double>(p, y, t); }
 
-std::vector<Jet> field_series(const Problem& p, const std::vector<Jet>& y, const Jet&) {
-  return eval_field<Jet>(p, y);
+std::vector<Jet> field_series(const Problem& p, const std::vector<Jet>& y, const Jet& t) {
+  return eval_field<Jet>(p, y, t);
 }
 
 Mat jacobian(const Problem& p, const Vec& y, double) {
@@ -217,6 +222,9 @@ Mat jacobian(const Problem& p, const Vec& y, double) {
       }
       break;
     }
+    case kPole:
+      j(0, 0) = 0.0;
+      break;
     case kAffine:
       for (int r = 0; r < d; ++r)
         for (int c = 0; c < d; ++c) j(r, c) = p.params[static_cast<std::size_t>(r * d + c)];
@@ -255,6 +263,9 @@ Problem make_problem(int kind) {
       p.y0.insert(p.y0.end(), vy0, vy0 + kBodies);
       break;
     }
+    case kPole:  // test_statespace.cpp:123-139 restated as a time pole at t = a
+      p.dim = 1, p.t_end = 1.0, p.y0 = {0.0}, p.params = {0.75};
+      break;
     default:
       throw InvalidInputError("unknown problem kind");
   }

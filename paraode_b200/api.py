@@ -36,10 +36,11 @@ class SingularFactorError(SolverError):
 
 
 class LinearizationError(SolverError):
-    def __init__(self, what, time=0.0, index=0):
+    def __init__(self, what, time=0.0, index=0, iteration=0):
         super().__init__(what)
         self.time = time
         self.index = index
+        self.iteration = iteration
 
 
 class ScanError(SolverError):
@@ -64,7 +65,7 @@ def _raise(rc: int, st: A.Status):
     cls = _ERRORS.get(rc, SolverError)
     msg = st.msg.decode(errors="replace")
     if cls is LinearizationError:
-        raise LinearizationError(msg, st.time, st.index)
+        raise LinearizationError(msg, st.time, st.index, st.iteration)
     raise cls(msg)
 
 
@@ -420,6 +421,13 @@ def fitzhugh_nagumo(a=0.2, b=0.2, c=3.0):
 def pleiades():
     y0 = [3, 3, -1, -3, 2, -2, 2, 3, -3, 2, 0, 0, -4, 4, 0, 0, 0, 0, 0, 1.75, -1.5, 0, 0, 0, -1.25, 1, 0, 0]
     return InitialValueProblem(5, 28, 3.0, np.array(y0, dtype=np.float64), name="pleiades")
+
+
+def pole(a=0.75, t_end=1.0, y0=0.0):
+    """y' = 1 / (t - a): finite Taylor initialisation, non-finite field at t = a
+    (the reference's LinearizationError case, test_statespace.cpp:123-139)."""
+    return InitialValueProblem(7, 1, t_end, np.array([y0], dtype=np.float64), np.array([a], dtype=np.float64),
+                               name="pole")
 
 
 def affine(l, c, y0, t_end):

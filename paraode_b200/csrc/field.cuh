@@ -3,7 +3,9 @@
 // which cannot run on the GPU; problems are therefore registered kinds with
 // parameters, evaluated here per time step.  Field definitions follow
 // proj/src/problems.cpp:81-107 (logistic, rigid body, Van der Pol) plus the
-// FitzHugh-Nagumo, Pleiades and affine fields of SURVEY.md §8c.
+// FitzHugh-Nagumo, Pleiades and affine fields of SURVEY.md §8c, and the
+// test kind PODE_POLE (y' = 1 / (t - a): the reference's non-finite-field
+// case, test_statespace.cpp:123-139, with the pole on a grid node).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -18,11 +20,12 @@ struct DevProblem {
   double params[kMaxParams];
 };
 
-// f(y) and its Jacobian J(y) (row stride DMAX) of an autonomous field, for
-// d = p.dim <= DMAX.  Every index is static once DMAX is fixed (cases whose
+// f(y, t) and its Jacobian J(y) (row stride DMAX), for d = p.dim <= DMAX.
+// Only PODE_POLE reads t.  Every index is static once DMAX is fixed (cases whose
 // dimension exceeds DMAX are compiled out), so y/f/jac stay in registers.
 template <int DMAX>
-__device__ __forceinline__ void eval_field(const DevProblem& p, const double* y, double* f, double* jac) {
+__device__ __forceinline__ void eval_field(const DevProblem& p, const double* y, double* f, double* jac,
+                                           double t = 0.0) {
   const int d = p.dim;
   switch (p.kind) {
     case 1: {  // logistic (problems.cpp:83-88, 126-128)
@@ -98,6 +101,11 @@ __device__ __forceinline__ void eval_field(const DevProblem& p, const double* y,
           f[3 * B + i] = ay;
         }
       }
+      break;
+    }
+    case 7: {  // pole: y' = 1 / (t - a) (non-finite exactly at t = a)
+      f[0] = 1.0 / (t - p.params[0]);
+      jac[0] = 0.0;
       break;
     }
     default: {  // affine: y' = L y + c

@@ -151,6 +151,10 @@ inline Problem resolve_problem(const pode_problem& p) {
       if (q.params.empty()) q.params = {0.2, 0.2, 3.0};
       break;
     case PODE_PLEIADES: want_dim = 28; break;
+    case PODE_POLE:
+      want_dim = 1;
+      if (q.params.empty()) q.params = {0.75};
+      break;
     case PODE_AFFINE:
       want_dim = p.dim;
       if (int(q.params.size()) != p.dim * p.dim + p.dim)
@@ -165,10 +169,15 @@ inline Problem resolve_problem(const pode_problem& p) {
   return q;
 }
 
+// t: the time series (prior.cpp:131-133 passes Jet::variable(0)); only
+// PODE_POLE depends on it.
 template <typename S>
-std::vector<S> field_series(const Problem& p, const std::vector<S>& y) {
+std::vector<S> field_series(const Problem& p, const std::vector<S>& y, const S& t) {
   std::vector<S> out(size_t(p.dim), y[0]);
   switch (p.kind) {
+    case PODE_POLE:
+      out[0] = (y[0] * 0.0 + 1.0) / (t - p.params[0]);
+      break;
     case PODE_LOGISTIC:
       out[0] = y[0] * (1.0 - y[0]);
       break;
@@ -230,8 +239,10 @@ inline std::vector<double> taylor_init(const Problem& p, int nu) {
   const int d = p.dim;
   std::vector<Jet> y(static_cast<size_t>(d), Jet{nu});
   for (int i = 0; i < d; ++i) y[i] = Jet(nu, p.y0[i]);
+  Jet t_series(nu, 0.0);
+  if (nu >= 1) t_series.c[1] = 1.0;
   for (int k = 0; k + 1 <= nu; ++k) {
-    const std::vector<Jet> fy = field_series<Jet>(p, y);
+    const std::vector<Jet> fy = field_series<Jet>(p, y, t_series);
     for (int i = 0; i < d; ++i) {
       if (!std::isfinite(fy[i].c[k]))
         throw ApiError(PODE_ERR_INVALID_INPUT, "taylor_init: vector field is not finite at the initial point");

@@ -69,7 +69,7 @@ static __global__ void k_linearize(DevProblem prob, int nu, const double* eta, c
   const double* s = scale + (i + 1) * D;
   double y[DMAX], f[DMAX], jac[DMAX * DMAX];
   for (int r = 0; r < d; ++r) y[r] = e[r * b];
-  eval_field<DMAX>(prob, y, f, jac);
+  eval_field<DMAX>(prob, y, f, jac, grid[i + 1]);
   bool finite = true;
   for (int r = 0; r < d; ++r) finite &= isfinite(f[r]);
   if (!ek0)
@@ -310,7 +310,8 @@ struct IeksSetup {
 // marginals in fm / fc (rescaled coordinates).  Inherently sequential: the
 // linearisation point of step n depends on the filter up to step n.
 template <int D>
-__global__ void __launch_bounds__(32) k_eks_forward(DevChain ch, DevProblem prob, int nu, const double* scale,
+__global__ void __launch_bounds__(32) k_eks_forward(DevChain ch, DevProblem prob, int nu, const double* grid,
+                                                    const double* scale,
                                                     int ek0, double* fm, double* fc, DevError* err) {
   extern __shared__ double smem[];
   const Grp<D> g = make_group<D>(smem);
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(32) k_eks_forward(DevChain ch, DevProblem prob
     if (ok && g.r < d) {
       double y[D], fv[D], jac[D * D];
       for (int r = 0; r < d; ++r) y[r] = eta[r * b];
-      eval_field<D>(prob, y, fv, jac);
+      eval_field<D>(prob, y, fv, jac, grid[n + 1]);
       const int r = g.r;
       bool finite = isfinite(fv[r]);
       if (!ek0)
@@ -519,7 +520,7 @@ struct IeksEngine {
     cuda_check(cudaFuncSetAttribute(k_eks_forward<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_smem),
                "eks smem");
     reset_error(ctx);
-    k_eks_forward<D><<<1, 32, fwd_smem, st>>>(ch, s.prob, s.nu, s.scale, cfg.linearization, fm, fc, err);
+    k_eks_forward<D><<<1, 32, fwd_smem, st>>>(ch, s.prob, s.nu, s.grid, s.scale, cfg.linearization, fm, fc, err);
     note_launch(ctx, "eks_forward");
     check_linearization(ctx, s, 1, 0, "eks_solve");
     // rts_smooth_pass of the sequential filter (sequential.cpp:105-132) as the reverse scan

@@ -158,10 +158,10 @@ struct Model {
     double off[d];
     bool finite;
   };
-  __device__ static Lin linearize(const DevProblem& prob, const double (&y)[d], int ek0) {
+  __device__ static Lin linearize(const DevProblem& prob, const double (&y)[d], int ek0, double t) {
     Lin l;
     double f[d], jac[d * d];
-    eval_field<d>(prob, y, f, jac);
+    eval_field<d>(prob, y, f, jac, t);
     bool fin = true;
 #pragma unroll
     for (int j = 0; j < d; ++j) fin &= isfinite(f[j]);
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(const FastArgs
     // update at node k+1
     double ylin[d];  // (a one-step-ahead load costs pass A more in spills than it saves)
     gather_y<D, d>(a, lp, c, k + 1 - s, k + 1, ylin);
-    const typename M::Lin lin = M::linearize(a.prob, ylin, a.ek0);
+    const typename M::Lin lin = M::linearize(a.prob, ylin, a.ek0, a.prob.kind == 7 ? a.grid[k + 1] : 0.0);
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
     const typename M::Upd u = M::update(lin, tn, cm);
     bad_sing |= u.singular;
@@ -687,7 +687,7 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
 #pragma unroll
     for (int i = 0; i < d; ++i) ylin[i] = ynext[i];
     if (k + 1 < e) gather_y<D, d>(a, lp, c, k + 2 - s, k + 2, ynext);
-    const typename M::Lin lin = M::linearize(a.prob, ylin, a.ek0);
+    const typename M::Lin lin = M::linearize(a.prob, ylin, a.ek0, a.prob.kind == 7 ? a.grid[k + 1] : 0.0);
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
     const typename M::Upd u = M::update(lin, tn, cm);
     bad_sing |= u.singular;

@@ -77,10 +77,11 @@ ERRORS = {1: "InvalidInputError", 2: "DimensionError", 3: "SingularFactorError",
 
 
 class OracleError(RuntimeError):
-    def __init__(self, code, msg):
+    def __init__(self, code, msg, time=0.0, index=-1, iteration=0):
         super().__init__(f"{ERRORS.get(code, code)}: {msg}")
         self.code = code
         self.kind = ERRORS.get(code, "SolverError")
+        self.time, self.index, self.iteration = time, index, iteration
 
 
 _lib = None
@@ -122,7 +123,7 @@ def P(a):
 
 def _check(rc, st):
     if rc != 0:
-        raise OracleError(st.code, st.msg.decode(errors="replace"))
+        raise OracleError(st.code, st.msg.decode(errors="replace"), st.time, st.index, st.iteration)
 
 
 # ------------------------------------------------------------ containers ---
@@ -365,7 +366,7 @@ def rts(chain, mode=0):
                 stats=(stats.combine_invocations, stats.sequential_depth))
 
 
-KIND = {"logistic": 1, "rigidbody": 2, "vanderpol": 3, "fhn": 4, "pleiades": 5, "affine": 6}
+KIND = {"logistic": 1, "rigidbody": 2, "vanderpol": 3, "fhn": 4, "pleiades": 5, "affine": 6, "pole": 7}
 SHIPPED = {  # name: (kind, dim, t_end, y0)
     "logistic": (1, 1, 10.0, [0.01]),
     "rigidbody": (2, 3, 20.0, [1.0, 0.0, 0.9]),
