@@ -67,6 +67,16 @@ int32_t pode_max_state_dim(void);
 int64_t pode_kernel_launches(const pode_context* ctx);
 /* The CUDA stream (cudaStream_t) the context launches on. */
 void* pode_context_stream(pode_context* ctx);
+/* Per-context engine options (replace process-wide environment knobs, so
+ * concurrent contexts do not see each other's settings):
+ *   PODE_OPT_CHUNK_LEN  time steps per chunk of the fused IEKS engines
+ *                       (0 = automatic: ~256 chunks per SM; clamped to [2, N];
+ *                       N = one chunk = the sequential Kalman recursion, seq_ieks)
+ *   PODE_OPT_ENGINE     0 = automatic, 1 = fused engines only (PODE_ERR_UNSUPPORTED
+ *                       when none serves the state), 2 = the element engine
+ * Returns PODE_OK or PODE_ERR_INVALID_INPUT. */
+typedef enum { PODE_OPT_CHUNK_LEN = 1, PODE_OPT_ENGINE = 2 } pode_option;
+int pode_context_set_option(pode_context* ctx, int32_t option, int64_t value);
 /* Per-kernel CUDA-event timing on the context stream (instrumentation):
  * pode_profile(ctx, 1) clears and starts recording, pode_profile(ctx, 0)
  * stops; pode_profile_read writes "kernel launches total_ms" lines into buf

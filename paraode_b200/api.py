@@ -91,6 +91,22 @@ class Context:
     def stream(self) -> int:
         return int(self._lib.pode_context_stream(self._h) or 0)
 
+    OPT_CHUNK_LEN, OPT_ENGINE = 1, 2
+    ENGINES = {"auto": 0, "fused": 1, "elements": 2}
+
+    def set_option(self, option: int, value: int):
+        """pode_context_set_option: per-context engine knobs (chunk length of
+        the fused engines; engine choice auto / fused / elements)."""
+        rc = self._lib.pode_context_set_option(self._h, int(option), int(value))
+        if rc != 0:
+            raise InvalidInputError(f"pode_context_set_option({option}, {value}) rejected")
+
+    def set_chunk_len(self, steps: int):
+        self.set_option(self.OPT_CHUNK_LEN, steps)
+
+    def set_engine(self, name: str):
+        self.set_option(self.OPT_ENGINE, self.ENGINES[name])
+
     def profile(self, enable: bool):
         """Start (clear) / stop per-kernel CUDA-event timing on the context stream."""
         self._lib.pode_profile(self._h, int(enable))
@@ -521,7 +537,7 @@ def eks_solve(ivp: InitialValueProblem, prior: IwpPrior, grid: Sequence[float], 
 
 
 # ---------------------------------------------------- batched solves ---
-_batch_ctxs: list = []
+_batch_pools: dict = {}  # device -> (lock, [Context]); a batch call holds its device's lock
 
 
 def para_ieks_batch(problems: Sequence[InitialValueProblem], prior: IwpPrior, grid: Sequence[float],
@@ -537,13 +553,21 @@ def para_ieks_batch(problems: Sequence[InitialValueProblem], prior: IwpPrior, gr
     if not problems:
         return []
     streams = max(1, min(int(streams), len(problems)))
-    while len(_batch_ctxs) < streams:
-        _batch_ctxs.append(Context(device))
+    lock, ctxs = _batch_pools.setdefault(int(device), (threading.Lock(), []))
+    with lock:  # contexts are not reentrant: one batch per device at a time
+        while len(ctxs) < streams:
+            ctxs.append(Context(device))
+        return _run_batch(problems, prior, grid, config, want_cov, ctxs[:streams])
+
+
+def _run_batch(problems, prior, grid, config, want_cov, ctxs):
+    import threading
+    streams = len(ctxs)
     out = [None] * len(problems)
     errors = []
 
     def worker(w):
-        ctx = _batch_ctxs[w]
+        ctx = ctxs[w]
         for i in range(w, len(problems), streams):
             try:
                 out[i] = para_ieks(problems[i], prior, grid, config, want_cov=want_cov, ctx=ctx)

@@ -22,7 +22,6 @@ from __future__ import annotations
 import argparse
 import json
 import math
-import os
 import statistics
 import sys
 import time
@@ -96,28 +95,26 @@ def _solver(method: str):
     if method not in METHODS:
         raise UsageError(f"unknown method '{method}' (expected {', '.join(METHODS)})")
     import paraode_b200 as P
+    ctxs = {}  # one dedicated context per engine setting, reused across runs
 
-    def with_env(key, value, fn):
-        old = os.environ.get(key)
-        os.environ[key] = value
-        try:
-            return fn()
-        finally:
-            if old is None:
-                del os.environ[key]
-            else:
-                os.environ[key] = old
+    def engine_ctx(engine, chunk=0):
+        if engine not in ctxs:
+            ctxs[engine] = P.Context()
+            ctxs[engine].set_engine(engine)
+        ctxs[engine].set_chunk_len(chunk)
+        return ctxs[engine]
 
     def run(prob, prior, grid, config):
         if method == "eks":  # bench.cpp:139
             return P.eks_solve(prob, prior, grid, config.linearization)
         if method == "ieks":  # bench.cpp:138: seq_ieks = the same iterates, time-sequential
-            # one chunk: a single lane thread runs every Kalman fold in time
-            # order (fused engine, D <= 9; larger states use the element engine)
-            return with_env("PODE_CHUNK", str(max(2, len(grid) - 1)),
-                            lambda: P.para_ieks(prob, prior, grid, config))
+            # one chunk on a dedicated context: a single lane thread runs every
+            # Kalman fold in time order; states no fused engine serves are
+            # rejected (UnsupportedError) rather than run on the parallel
+            # element engine under this label
+            return P.para_ieks(prob, prior, grid, config, ctx=engine_ctx("fused", max(2, len(grid) - 1)))
         if method == "paraieks-elements":
-            return with_env("PODE_IEKS_ENGINE", "elements", lambda: P.para_ieks(prob, prior, grid, config))
+            return P.para_ieks(prob, prior, grid, config, ctx=engine_ctx("elements"))
         return P.para_ieks(prob, prior, grid, config)
     return run
 

@@ -416,6 +416,22 @@ int64_t pode_kernel_launches(const pode_context* ctx) { return ctx ? ctx->launch
 
 void* pode_context_stream(pode_context* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
+int pode_context_set_option(pode_context* ctx, int32_t option, int64_t value) {
+  if (ctx == nullptr) return PODE_ERR_INVALID_INPUT;
+  switch (option) {
+    case PODE_OPT_CHUNK_LEN:
+      if (value < 0) return PODE_ERR_INVALID_INPUT;
+      ctx->opt_chunk = value;
+      return PODE_OK;
+    case PODE_OPT_ENGINE:
+      if (value < 0 || value > 2) return PODE_ERR_INVALID_INPUT;
+      ctx->opt_engine = int(value);
+      return PODE_OK;
+    default:
+      return PODE_ERR_INVALID_INPUT;
+  }
+}
+
 int pode_combine_filtering(pode_context* ctx, int64_t count, int32_t D, pode_filtering_elements lhs,
                            pode_filtering_elements rhs, pode_filtering_elements out, int32_t location,
                            pode_status* status) {

@@ -82,6 +82,9 @@ struct pode_context {
   unsigned long long* h_err = nullptr;  // pinned mirror
   double* h_scalars = nullptr;          // pinned scalars (reductions)
   int64_t launches = 0;
+  // pode_context_set_option (0 = automatic / environment default)
+  int64_t opt_chunk = 0;
+  int opt_engine = 0;
   // Instantiated device-side IEKS loops (fast_driver.cuh), reused while the
   // captured kernel arguments (key) and the workspace generation match.
   struct GraphSlot {

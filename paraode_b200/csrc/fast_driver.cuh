@@ -107,11 +107,27 @@ struct FastEngine {
       const int64_t l0 = ctx->launches;
       cuda_check(cudaStreamBeginCaptureToGraph(st, g_body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed),
                  "capture");
-      body(true, h);
-      cuda_check(cudaStreamEndCapture(st, &g_body), "end capture");
-      slot.per_iter = ctx->launches - l0;
-      ctx->launches = l0;
-      cuda_check(cudaGraphInstantiate(&slot.exec, slot.graph, 0), "instantiate");
+      try {
+        body(true, h);
+        cuda_check(cudaStreamEndCapture(st, &g_body), "end capture");
+        slot.per_iter = ctx->launches - l0;
+        ctx->launches = l0;
+        cuda_check(cudaGraphInstantiate(&slot.exec, slot.graph, 0), "instantiate");
+      } catch (...) {
+        // leave the stream out of capture mode and drop the half-built graph,
+        // so the context stays usable for the next solve
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+          cudaGraph_t dropped = nullptr;
+          cudaStreamEndCapture(st, &dropped);
+        }
+        cudaGetLastError();
+        if (slot.exec) cudaGraphExecDestroy(slot.exec);
+        if (slot.graph) cudaGraphDestroy(slot.graph);
+        slot = pode_context::GraphSlot{};
+        ctx->launches = l0;
+        throw;
+      }
       slot.key = key;
     }
     cuda_check(cudaGraphLaunch(slot.exec, st), "graph launch");
@@ -159,8 +175,10 @@ struct FastEngine {
 
   // One chunk per thread, ~256 resident threads per SM.
   static int chunk_len(pode_context* ctx, int64_t N) {
-    const char* env = std::getenv("PODE_CHUNK");  // unset or empty: the default below
-    if (env && *env) return std::max(2, std::atoi(env));
+    if (ctx->opt_chunk > 0)  // pode_context_set_option(PODE_OPT_CHUNK_LEN)
+      return static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(ctx->opt_chunk, std::max<int64_t>(N, 2))));
+    const char* env = std::getenv("PODE_CHUNK");  // developer override; unset or empty: the default below
+    if (env && *env) return static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(std::atoll(env), std::max<int64_t>(N, 2))));
     const int64_t target = int64_t(ctx->sm_count) * 256;
     const int64_t L = (N + target - 1) / target;
     return static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(L, 4096)));

@@ -47,7 +47,7 @@ constexpr bool kFastOk = (d <= 3) && (DD % d == 0) && (DD / d >= 2) && (DD / d <
 void ik(pode_context* c, const host::Problem& p, const pode_prior& pr, const double* g, int64_t n1,
         const pode_ieks_config& cfg, double* m, double* cv, double* sm, double* sc, IeksResult* out) {
   const char* env = std::getenv("PODE_IEKS_ENGINE");
-  const bool elements = env != nullptr && std::string(env) == "elements";
+  const bool elements = c->opt_engine == 2 || (c->opt_engine == 0 && env != nullptr && std::string(env) == "elements");
   if (!elements) {
     switch (pr.dim) {
       case 1:
@@ -71,6 +71,9 @@ void ik(pode_context* c, const host::Problem& p, const pode_prior& pr, const dou
       default:
         break;
     }
+    if (c->opt_engine == 1)
+      throw ApiError(PODE_ERR_UNSUPPORTED, "ieks: no fused engine serves state dimension " + std::to_string(kD) +
+                                               " with d = " + std::to_string(pr.dim));
   }
   *out = IeksEngine<kD>::run(c, p, pr, g, n1, cfg, m, cv, sm, sc);
 }
