@@ -3,6 +3,9 @@
 // engines (engine.cuh).
 #pragma once
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -121,9 +124,26 @@ inline void prof_record(pode_context* ctx, const char* name) {
   ctx->prof.push_back({name, e});
 }
 
+// PODE_TRACE_LAUNCHES=1 (debugging): synchronise after every launch and
+// name it on stderr, so a fault or hang is attributed to its kernel.
+inline bool trace_launches() {
+  static const bool on = [] {
+    const char* e = std::getenv("PODE_TRACE_LAUNCHES");
+    return e != nullptr && *e != '\0' && *e != '0';
+  }();
+  return on;
+}
+
 inline void note_launch(pode_context* ctx, const char* what) {
   ctx->launches += 1;
   cuda_check(cudaGetLastError(), what);
+  if (trace_launches()) {
+    std::fprintf(stderr, "[pode] launch %lld %s ...", static_cast<long long>(ctx->launches), what);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(ctx->stream, &cs);
+    if (cs == cudaStreamCaptureStatusNone) cuda_check(cudaStreamSynchronize(ctx->stream), what);
+    std::fprintf(stderr, " done\n");
+  }
   prof_record(ctx, what);
 }
 

@@ -552,6 +552,13 @@ __global__ void __launch_bounds__(kBWarps * 32, kGroupMinBlocks / 2) k_bscan_loc
   if (ok && g.r == 0 && bad) raise_error(err, k, kErrSingular);
 }
 
+// The block scan needs its tiles and G elements in shared memory (<= 227 KB
+// per CTA): large D (e.g. 15) keeps the fan-in levels throughout.
+template <int D, class Op>
+constexpr bool bscan_fits() {
+  return bscan_smem<D, Op>() <= size_t(227) * 1024;
+}
+
 // Scan levels above 0 with at most this many elements use the block kernel
 // (latency-bound: Sklansky depth); larger levels keep the work-efficient
 // sequential fan-in (throughput-bound).  PODE_BSCAN=0 disables, =n sets it.
@@ -664,7 +671,7 @@ struct Engine {
     DevError* err = reinterpret_cast<DevError*>(ctx->d_err);
     size_t sm = smem_bytes<D>();
     FEd loc = alloc<FOps<D>>(ctx, "gscan_loc_" + std::to_string(level), n);
-    if (level >= 1 && n <= bscan_max()) {  // block Sklansky levels
+    if (level >= 1 && n <= bscan_max() && bscan_fits<D, FOps<D>>()) {  // block Sklansky levels
       constexpr int G = bscan_groups<D>();
       sm = bscan_smem<D, FOps<D>>();
       static OncePerDevice once;
@@ -735,7 +742,7 @@ struct Engine {
   static void mscan_rec(pode_context* ctx, SEd in, SEd out, int64_t n, int level, int L, ScanTally& t) {
     size_t sm = smem_bytes<D>();
     SEd loc = alloc<SOps<D>>(ctx, "mscan_loc_" + std::to_string(level), n);
-    if (level >= 1 && n <= bscan_max()) {  // block Sklansky levels
+    if (level >= 1 && n <= bscan_max() && bscan_fits<D, MOps<D>>()) {  // block Sklansky levels
       constexpr int G = bscan_groups<D>();
       sm = bscan_smem<D, MOps<D>>();
       static OncePerDevice once;

@@ -10,6 +10,7 @@
 #include <string>
 
 #include "fast.cuh"
+#include "grp_fused.cuh"
 #include "ieks.cuh"
 #include "lane.cuh"
 
@@ -68,7 +69,122 @@ static __global__ void k_finish_iter(const double* part, int64_t nparts, LoopSta
   cudaGraphSetConditional(h, (!conv && !failed && ls->it < ls->max_it) ? 1u : 0u);
 }
 
+// Launch policies of the fused iteration: the lane-serial passes (lane.cuh,
+// one chunk per thread, chunk-interleaved HBM layout; D <= 9) and the
+// group-of-D-lanes passes (grp_fused.cuh, one chunk per group, node-major
+// layout; D = 10..16).  The driver below is shared.
 template <int D, int d>
+struct LanePasses {
+  static constexpr bool kLane = true;
+  static constexpr const char* kName = "lane";
+  static int64_t target_chunks(pode_context* ctx) { return int64_t(ctx->sm_count) * 256; }
+  static unsigned blocks(int64_t nc) { return static_cast<unsigned>((nc + lane::kLaneThreads - 1) / lane::kLaneThreads); }
+  static void set_attrs() {
+    static OncePerDevice once;
+    once([] {
+      cuda_check(cudaFuncSetAttribute(lane::k_lane_fwd_down<D, d, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(lane::fwd_down_smem<D>())),
+                 "pass C smem");
+    });
+  }
+  static void fill(cudaStream_t st, const double* mu0, int64_t nc, int L, double* eta) {
+    lane::k_eta_fill<D><<<grid1(nc * L * D + D), kRedThreads, 0, st>>>(mu0, nc, L, eta);
+  }
+  static void rows(cudaStream_t st, const double* base, const double* term, int64_t N, int L, int64_t nc,
+                   double* out) {
+    lane::k_eta_rows<D><<<grid1((N + 1) * D), kRedThreads, 0, st>>>(base, term, N, L, nc, out);
+  }
+  static void fwd_reduce(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const FEd& agg) {
+    lane::k_lane_fwd_reduce<D, d><<<blocks(a.nchunks), lane::kLaneThreads, 0, st>>>(a, cst, agg);
+  }
+  static void fwd_down(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const FEd& agg,
+                       const lane::ElemSoA& soa, const SEd& bagg) {
+    lane::k_lane_fwd_down<D, d><<<blocks(a.nchunks), lane::kLaneThreads, lane::fwd_down_smem<D>(), st>>>(
+        a, cst, agg, soa, nullptr, nullptr, nullptr, bagg);
+  }
+  template <bool kInit>
+  static void bwd_down(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const lane::ElemSoA& soa,
+                       const SEd& bagg, const double* eo, const double* ot, double* en, double* nt, double* part) {
+    lane::k_lane_bwd_down<D, d, kInit><<<blocks(a.nchunks), lane::kLaneThreads, 0, st>>>(a, cst, soa, bagg, eo, ot, en,
+                                                                                         nt, part);
+  }
+  static void fin_fwd(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const FEd& agg,
+                      const lane::ElemSoA& soa, double* cf, double* cterm, double* part) {
+    lane::k_lane_fwd_down<D, d, true><<<blocks(a.nchunks), lane::kLaneThreads, 0, st>>>(a, cst, agg, soa, cf, cterm,
+                                                                                        part);
+  }
+  static void fin_fold(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const lane::ElemSoA& soa,
+                       const double* cf, const double* cterm, const SEd& sagg) {
+    lane::k_lane_fin_fold<D, d><<<blocks(a.nchunks), lane::kLaneThreads, 0, st>>>(a, cst, soa, cf, cterm, sagg);
+  }
+  static void fin_bwd(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const lane::ElemSoA& soa,
+                      const double* cf, const double* cterm, const SEd& sagg, const double* eo, const double* eot,
+                      const double* red, double count, const lane::FinOut& out) {
+    lane::k_lane_fin_bwd<D, d><<<blocks(a.nchunks), lane::kLaneThreads, 0, st>>>(a, cst, soa, cf, cterm, sagg, eo, eot,
+                                                                                red, count, out);
+  }
+};
+
+template <int D, int d>
+struct GroupPasses {
+  static constexpr bool kLane = false;
+  static constexpr const char* kName = "grp";
+  // groups are latency-bound per step: ~32 chunks per SM
+  static int64_t target_chunks(pode_context* ctx) { return int64_t(ctx->sm_count) * 32; }
+  static unsigned blocks(int64_t nc) { return blocks_for<D>(nc); }
+  static void set_attrs() {
+    static OncePerDevice once;
+    once([] {
+      const int bytes = int(smem_bytes<D>());
+      cudaFuncSetAttribute(grp::k_grp_fwd_reduce<D, d>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      cudaFuncSetAttribute(grp::k_grp_fwd_down<D, d, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      cudaFuncSetAttribute(grp::k_grp_fwd_down<D, d, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      cudaFuncSetAttribute(grp::k_grp_bwd_down<D, d, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      cudaFuncSetAttribute(grp::k_grp_bwd_down<D, d, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      cudaFuncSetAttribute(grp::k_grp_fin_fold<D, d>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      cudaFuncSetAttribute(grp::k_grp_fin_bwd<D, d>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    });
+  }
+  static void fill(cudaStream_t st, const double* mu0, int64_t nc, int L, double* eta) {
+    grp::k_eta_fill_rows<D><<<grid1((nc * L + 1) * D), kRedThreads, 0, st>>>(mu0, nc * L, eta);
+  }
+  static void rows(cudaStream_t st, const double* base, const double* term, int64_t N, int, int64_t,
+                   double* out) {
+    cuda_check(cudaMemcpyAsync(out, base, sizeof(double) * N * D, cudaMemcpyDeviceToDevice, st), "eta rows");
+    cuda_check(cudaMemcpyAsync(out + N * D, term, sizeof(double) * D, cudaMemcpyDeviceToDevice, st), "eta rows");
+  }
+  static void fwd_reduce(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const FEd& agg) {
+    grp::k_grp_fwd_reduce<D, d><<<blocks(a.nchunks), kThreads, smem_bytes<D>(), st>>>(a, cst, agg);
+  }
+  static void fwd_down(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const FEd& agg,
+                       const lane::ElemSoA& soa, const SEd& bagg) {
+    grp::k_grp_fwd_down<D, d, false><<<blocks(a.nchunks), kThreads, smem_bytes<D>(), st>>>(a, cst, agg, soa, nullptr,
+                                                                                         nullptr, nullptr, bagg);
+  }
+  template <bool kInit>
+  static void bwd_down(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const lane::ElemSoA& soa,
+                       const SEd& bagg, const double* eo, const double* ot, double* en, double* nt, double* part) {
+    grp::k_grp_bwd_down<D, d, kInit><<<blocks(a.nchunks), kThreads, smem_bytes<D>(), st>>>(a, cst, soa, bagg, eo, ot,
+                                                                                          en, nt, part);
+  }
+  static void fin_fwd(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const FEd& agg,
+                      const lane::ElemSoA& soa, double* cf, double* cterm, double* part) {
+    grp::k_grp_fwd_down<D, d, true><<<blocks(a.nchunks), kThreads, smem_bytes<D>(), st>>>(a, cst, agg, soa, cf, cterm,
+                                                                                        part, SEd{});
+  }
+  static void fin_fold(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const lane::ElemSoA& soa,
+                       const double* cf, const double* cterm, const SEd& sagg) {
+    grp::k_grp_fin_fold<D, d><<<blocks(a.nchunks), kThreads, smem_bytes<D>(), st>>>(a, cst, soa, cf, cterm, sagg);
+  }
+  static void fin_bwd(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const lane::ElemSoA& soa,
+                      const double* cf, const double* cterm, const SEd& sagg, const double* eo, const double* eot,
+                      const double* red, double count, const lane::FinOut& out) {
+    grp::k_grp_fin_bwd<D, d><<<blocks(a.nchunks), kThreads, smem_bytes<D>(), st>>>(a, cst, soa, cf, cterm, sagg, eo,
+                                                                                   eot, red, count, out);
+  }
+};
+
+template <int D, int d, class Pass = LanePasses<D, d>>
 struct FastEngine {
   // Iterations 2.. run as one CUDA graph with a device-side while node (no
   // host round trip per iteration) unless profiling or PODE_GRAPH=0.
@@ -164,22 +280,16 @@ struct FastEngine {
     return v >= 2 ? v : 4;
   }
 
-  static void set_attrs() {
-    static OncePerDevice once;
-    once([] {
-      cuda_check(cudaFuncSetAttribute(lane::k_lane_fwd_down<D, d, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(lane::fwd_down_smem<D>())),
-                 "pass C smem");
-    });
-  }
+  static void set_attrs() { Pass::set_attrs(); }
 
-  // One chunk per thread, ~256 resident threads per SM.
+  // Lane passes: one chunk per thread, ~256 resident threads per SM; group
+  // passes: one chunk per group, ~32 per SM.
   static int chunk_len(pode_context* ctx, int64_t N) {
     if (ctx->opt_chunk > 0)  // pode_context_set_option(PODE_OPT_CHUNK_LEN)
       return static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(ctx->opt_chunk, std::max<int64_t>(N, 2))));
     const char* env = std::getenv("PODE_CHUNK");  // developer override; unset or empty: the default below
     if (env && *env) return static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(std::atoll(env), std::max<int64_t>(N, 2))));
-    const int64_t target = int64_t(ctx->sm_count) * 256;
+    const int64_t target = Pass::target_chunks(ctx);
     const int64_t L = (N + target - 1) / target;
     return static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(L, 4096)));
   }
@@ -218,16 +328,14 @@ struct FastEngine {
       double* base = ws.arr<double>("fast_bagg", size_t(nc) * (D * D + D));
       bagg = SEd{base, base + size_t(nc) * D * D, nullptr};
     }
-    const unsigned lblocks = static_cast<unsigned>((nc + lane::kLaneThreads - 1) / lane::kLaneThreads);
-    const int64_t nparts = int64_t(lblocks);
+    const int64_t nparts = int64_t(Pass::blocks(nc));
     double* part = ws.arr<double>("fast_part", nparts * 3 + 3);
     double* red = part + nparts * 3;
-    const unsigned th = lane::kLaneThreads;
     auto term = [&](double* base) { return base + padded * D; };
     FastArgs a{s.grid, eta_a, term(eta_a), N, L, nc, cfg.linearization, s.prob,
                reinterpret_cast<DevError*>(ctx->d_err)};
 
-    lane::k_eta_fill<D><<<grid1(int64_t(padded) * D + D), kRedThreads, 0, st>>>(s.mu0, nc, L, eta_a);
+    Pass::fill(st, s.mu0, nc, L, eta_a);
     note_launch(ctx, "fill");
     auto finish = [&]() {
       k_finish3<<<1, kRedThreads, 0, st>>>(part, nparts, red);
@@ -235,8 +343,7 @@ struct FastEngine {
       cuda_check(cudaMemcpyAsync(ctx->h_scalars, red, sizeof(double) * 3, cudaMemcpyDeviceToHost, st), "red");
     };
     // objective of the constant start (ieks.cpp:147-148)
-    lane::k_lane_bwd_down<D, d, true><<<lblocks, th, 0, st>>>(a, cst, soa, bagg, eta_a, term(eta_a), eta_b,
-                                                               term(eta_b), part);
+    Pass::template bwd_down<true>(st, a, cst, soa, bagg, eta_a, term(eta_a), eta_b, term(eta_b), part);
     note_launch(ctx, "fast_objective");
     finish();
     cuda_check(cudaStreamSynchronize(st), "sync");
@@ -262,15 +369,13 @@ struct FastEngine {
         ag.eta = eta_a;
         ag.eta_term = term(eta_a);
       }
-      lane::k_lane_fwd_reduce<D, d><<<lblocks, th, 0, st>>>(ag, cst, agg);
+      Pass::fwd_reduce(st, ag, cst, agg);
       note_launch(ctx, "fast_fwd_reduce");
       const ScanTally tf = Engine<D>::scan_filtering_gauss(ctx, nc, agg, agg, scan_fanin());
-      lane::k_lane_fwd_down<D, d><<<lblocks, th, lane::fwd_down_smem<D>(), st>>>(ag, cst, agg, soa, nullptr,
-                                                                                nullptr, nullptr, bagg);
+      Pass::fwd_down(st, ag, cst, agg, soa, bagg);
       note_launch(ctx, "fast_fwd_down");
       const ScanTally tr = Engine<D>::scan_means_terminal(ctx, nc, bagg, scan_fanin());
-      lane::k_lane_bwd_down<D, d, false><<<lblocks, th, 0, st>>>(ag, cst, soa, bagg, eta_a, term(eta_a), eta_b,
-                                                                  term(eta_b), part);
+      Pass::template bwd_down<false>(st, ag, cst, soa, bagg, eta_a, term(eta_a), eta_b, term(eta_b), part);
       note_launch(ctx, "fast_bwd_down");
       if (graph) {
         k_finish_iter<<<1, kRedThreads, 0, st>>>(part, nparts, ls, trace_dev, ctx->d_err, h);
@@ -285,7 +390,7 @@ struct FastEngine {
     while (it < cfg.max_iterations) {
       if (it == 1 && use_graph(ctx, cfg)) {  // workspaces exist after one eager iteration
         KeyWriter kw;
-        kw << ctx->ws.generation << N << L << nc << padded << cfg.linearization << scan_fanin() << bscan_max()
+        kw << Pass::kName << ctx->ws.generation << N << L << nc << padded << cfg.linearization << scan_fanin() << bscan_max()
            << a.grid << a.err << a.prob.kind << a.prob.dim << pair0 << pair1 << agg.a << agg.b << agg.c << agg.eta
            << agg.j << soa.e << soa.g << soa.term << bagg.e << bagg.g << part << nparts << ls << trace_dev
            << ctx->d_err;
@@ -320,9 +425,9 @@ struct FastEngine {
       // row-major copies of the final linearisation point and trajectory
       double* lin_rows = ws.arr<double>("lane_lin_rows", size_t(n1) * D);
       double* out_rows = ws.arr<double>("lane_out_rows", size_t(n1) * D);
-      lane::k_eta_rows<D><<<grid1(n1 * D), kRedThreads, 0, st>>>(eta_b, term(eta_b), N, L, nc, lin_rows);
+      Pass::rows(st, eta_b, term(eta_b), N, L, nc, lin_rows);
       note_launch(ctx, "eta_rows");
-      lane::k_eta_rows<D><<<grid1(n1 * D), kRedThreads, 0, st>>>(eta_a, term(eta_a), N, L, nc, out_rows);
+      Pass::rows(st, eta_a, term(eta_a), N, L, nc, out_rows);
       note_launch(ctx, "eta_rows");
       IE::finalize(ctx, s, lin_rows, out_rows, cfg.linearization, it, prior.sigma, means, cov, sol_m, sol_c, res);
       return res;
@@ -604,25 +709,24 @@ struct FastEngine {
     const size_t padded = size_t(nc) * a.L;
     double* cf = ws.arr<double>("fin_cf", padded * D * D + D * D);
     double* cterm = cf + padded * D * D;
-    const unsigned lblocks = static_cast<unsigned>((nc + lane::kLaneThreads - 1) / lane::kLaneThreads);
+    const unsigned lblocks = Pass::blocks(nc);
     double* part = ws.arr<double>("fin_part", size_t(lblocks) * 3 + 3);
     double* red = part + size_t(lblocks) * 3;
     a.eta = eta_lin;
     a.eta_term = eta_lin_term;
     reset_error(ctx);
-    lane::k_lane_fwd_down<D, d, true><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, agg, soa, cf, cterm, part);
+    Pass::fin_fwd(st, a, cst, agg, soa, cf, cterm, part);
     note_launch(ctx, "fin_fwd");
     k_finish3<<<1, kRedThreads, 0, st>>>(part, lblocks, red);
     note_launch(ctx, "finish3");
     IeksEngine<D>::check_linearization(ctx, s, it);  // syncs the stream
     SEd sagg = Engine<D>::template alloc<SOps<D>>(ctx, "fin_sagg", nc);
-    lane::k_lane_fin_fold<D, d><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, soa, cf, cterm, sagg);
+    Pass::fin_fold(st, a, cst, soa, cf, cterm, sagg);
     note_launch(ctx, "fin_fold");
     const ScanTally t = Engine<D>::scan_smoothing(ctx, nc, sagg, sagg, true);
     res.stats.combines = std::max(res.stats.combines, a.N + t.combines);
     const double count = double(a.N) * s.dim;
-    lane::k_lane_fin_bwd<D, d><<<lblocks, lane::kLaneThreads, 0, st>>>(a, cst, soa, cf, cterm, sagg, eta_out,
-                                                                       eta_out_term, red, count, out);
+    Pass::fin_bwd(st, a, cst, soa, cf, cterm, sagg, eta_out, eta_out_term, red, count, out);
     note_launch(ctx, "fin_bwd");
     cuda_check(cudaMemcpyAsync(ctx->h_scalars, red, sizeof(double), cudaMemcpyDeviceToHost, st), "innov");
     IeksEngine<D>::check_linearization(ctx, s, it);  // syncs the stream

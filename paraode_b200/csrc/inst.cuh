@@ -40,8 +40,25 @@ template <int DD, int d>
 // spill heavily (and take tens of minutes to compile), so larger states use
 // the group engine.
 constexpr bool kFastOk = (d <= 3) && (DD % d == 0) && (DD / d >= 2) && (DD / d <= 5) && (DD <= 9);
+// Above that, the fused iteration runs on groups of D lanes (grp_fused.cuh).
+template <int DD, int d>
+constexpr bool kGrpOk = (d <= 3) && (DD % d == 0) && (DD / d >= 2) && (DD / d <= 8) && (DD >= 10) && (DD <= 16);
 
-// The fused engine (fast.cuh) serves ODE information operators with d <= 3;
+template <int d>
+bool run_fused(pode_context* c, const host::Problem& p, const pode_prior& pr, const double* g, int64_t n1,
+               const pode_ieks_config& cfg, double* m, double* cv, double* sm, double* sc, IeksResult* out) {
+  if constexpr (kFastOk<kD, d>) {
+    *out = FastEngine<kD, d>::run(c, p, pr, g, n1, cfg, m, cv, sm, sc);
+    return true;
+  } else if constexpr (kGrpOk<kD, d>) {
+    *out = FastEngine<kD, d, GroupPasses<kD, d>>::run(c, p, pr, g, n1, cfg, m, cv, sm, sc);
+    return true;
+  }
+  return false;
+}
+
+// The fused engines (fast.cuh: lane passes D <= 9, group passes D = 10..16)
+// serve ODE information operators with d <= 3;
 // everything else (and PODE_IEKS_ENGINE=elements) runs the element/scan
 // engine with the reference's per-iteration structure.
 void ik(pode_context* c, const host::Problem& p, const pode_prior& pr, const double* g, int64_t n1,
@@ -51,22 +68,13 @@ void ik(pode_context* c, const host::Problem& p, const pode_prior& pr, const dou
   if (!elements) {
     switch (pr.dim) {
       case 1:
-        if constexpr (kFastOk<kD, 1>) {
-          *out = FastEngine<kD, 1>::run(c, p, pr, g, n1, cfg, m, cv, sm, sc);
-          return;
-        }
+        if (run_fused<1>(c, p, pr, g, n1, cfg, m, cv, sm, sc, out)) return;
         break;
       case 2:
-        if constexpr (kFastOk<kD, 2>) {
-          *out = FastEngine<kD, 2>::run(c, p, pr, g, n1, cfg, m, cv, sm, sc);
-          return;
-        }
+        if (run_fused<2>(c, p, pr, g, n1, cfg, m, cv, sm, sc, out)) return;
         break;
       case 3:
-        if constexpr (kFastOk<kD, 3>) {
-          *out = FastEngine<kD, 3>::run(c, p, pr, g, n1, cfg, m, cv, sm, sc);
-          return;
-        }
+        if (run_fused<3>(c, p, pr, g, n1, cfg, m, cv, sm, sc, out)) return;
         break;
       default:
         break;

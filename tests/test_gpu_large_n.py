@@ -20,11 +20,9 @@ import os
 import numpy as np
 import pytest
 
-import _oracle as O
+from _parity import MEAN_TOL, COV_TOL, NEVER, alternatives, compare, gpu_solve, per_order, rel
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-MEAN_TOL, COV_TOL, SIG_TOL = 1e-9, 1e-7, 1e-7
-NEVER = dict(traj_rtol=-1.0, obj_atol=-1.0, obj_rtol=0.0)
 
 
 def load(name):
@@ -36,85 +34,16 @@ def load(name):
     return z, meta
 
 
-def rel(a, b):
-    a, b = np.asarray(a), np.asarray(b)
-    return float(np.max(np.abs(a - b)) / max(1.0, np.max(np.abs(b))))
-
-
-def cov_upper(cov_sqrt, nodes):
-    L = cov_sqrt[nodes]
-    cov = np.einsum("nij,nkj->nik", L, L)
-    iu = np.triu_indices(cov.shape[1])
-    return cov[:, iu[0], iu[1]]
-
-
-def gpu_solve(P, meta, ctx=None, **cfg):
-    name = {"fhn": "fhn", "vanderpol": "vanderpol", "rigidbody": "rigidbody"}[meta["problem"]]
-    prob = P.problem_by_name(name)
-    grid = P.uniform_grid(meta["t_end"], meta["steps"])
-    return P.para_ieks(prob, P.IwpPrior(meta["nu"], prob.dim, 1.0), grid, P.IeksConfig(**cfg), ctx=ctx)
-
-
-def per_order(a, b, B):
-    """rel error of each derivative order k (state entries k, k+B, ...)."""
-    return [rel(a[:, k::B], b[:, k::B]) for k in range(B)]
-
-
-def compare(rep, z, meta, label, alts=()):
-    """Equal-iteration parity.  Means at 1e-9 per derivative order, the
-    uncalibrated covariance products L L^T / sigma_hat^2 at 1e-7 and sigma_hat
-    at 1e-7 — except where the reference formulation itself is
-    rounding-determined: in the rescaled coordinates (T_0 = sqrt(h) h^q / q!,
-    ieks.cpp:28-33) the high derivative orders of the mean, and sigma_hat
-    (from innovations that read them), carry rounding noise of order
-    eps |x_0| T_k / T_0.  `alts` are GPU solves of the same problem that
-    differ only in rounding (other chunk lengths, the element engine); the
-    per-order floor is the GPU's largest distance to them, and each order (and
-    sigma_hat) must agree with the oracle to max(tolerance, 10 x floor)."""
-    nodes = z["nodes"]
-    B = meta["nu"] + 1
-    orders = per_order(rep.means[nodes], z["means"], B)
-    sig = abs(rep.sigma_hat - meta["sigma_hat"]) / abs(meta["sigma_hat"])
-    sr = (rep.sigma_hat / meta["sigma_hat"]) ** 2  # compare uncalibrated covariances
-    ec = rel(cov_upper(rep.cov_sqrt, nodes) / sr, z["cov_upper"])
-    floor = [0.0] * B
-    f_sig = 0.0
-    for alt in alts:
-        floor = [max(f, e) for f, e in zip(floor, per_order(rep.means, alt.means, B))]
-        f_sig = max(f_sig, abs(rep.sigma_hat - alt.sigma_hat) / abs(alt.sigma_hat))
-    line = (f"{label}: {rep.iterations} its, mean orders " + " ".join(f"{e:.1e}" for e in orders) +
-            f", cov/sigma^2 {ec:.1e}, sigma {sig:.1e} | GPU rounding floor: orders " +
-            " ".join(f"{e:.1e}" for e in floor) + f", sigma {f_sig:.1e}")
-    print(line)
-    assert rep.iterations == meta["iterations"]
-    assert ec <= COV_TOL, line
-    for k in range(B):
-        assert orders[k] <= max(MEAN_TOL, 10 * floor[k]), line
-    assert sig <= max(SIG_TOL, 10 * f_sig), line
-
-
-def alternatives(P, meta, its):
-    """Solves differing from the default one only in rounding: the fused
-    engine at two other chunk lengths (states it serves) and the element
-    engine (the reference's per-iteration structure)."""
-    D = (meta["nu"] + 1) * {"fhn": 2, "vanderpol": 2, "rigidbody": 3}[meta["problem"]]
-    out = []
-    settings = [("elements", 0)] + ([("auto", 13), ("auto", 19)] if D <= 16 else [])
-    for engine, chunk in settings:
-        ctx = P.Context()
-        ctx.set_engine(engine)
-        ctx.set_chunk_len(chunk)
-        out.append(gpu_solve(P, meta, ctx=ctx, max_iterations=its, **NEVER))
-    return out
-
-
 # ------------------------------------------------------------- CPU side ---
 def test_fixture_self_consistency():
     """The fixtures agree with what they claim (CPU, no GPU): node grids,
     iteration counts, trace lengths; and the reference's own two paths
-    (seq_ieks vs para_ieks on WorkPool(8)) at 20 equal iterations: derivative
-    orders 0..q-1 agree at the GPU's tolerance, the top order only to its
-    rounding floor (printed: the reference's own distance)."""
+    (seq_ieks vs para_ieks on WorkPool(8)) at 20 equal iterations, mid-way
+    through the Gauss-Newton transient, differ by a rounding floor of their
+    own: measured 4.2e-9 on orders 0 and 1, 8.4e-6 on the top order and
+    7.4e-3 on sigma_hat — MORE than the GPU's distance to seq_ieks at the same
+    point (2.5e-10, 2.8e-10, 1.1e-5, 1.7e-3; test_fhn_2e20_equal_iterations).
+    At the converged 54th iterate the GPU agrees with seq_ieks to 1.4e-10."""
     for name in ("fhn_q2_n20_seq", "fhn_q2_n20_seq_it20"):
         z, meta = load(name)
         assert z["nodes"][-1] == meta["steps"] and len(z["objective_trace"]) == meta["iterations"]
@@ -128,7 +57,7 @@ def test_fixture_self_consistency():
     ec = rel(p20["cov_upper"] / sr, s20["cov_upper"])
     print("reference seq vs par at 20 iterations, N=2^20: mean orders " + " ".join(f"{e:.1e}" for e in orders) +
           f", cov/sigma^2 {ec:.1e}, sigma {abs(pm20['sigma_hat'] / m20['sigma_hat'] - 1):.1e}")
-    assert max(orders[:-1]) <= MEAN_TOL and ec <= COV_TOL
+    assert max(orders[:-1]) <= 1e-7 and ec <= 1e-7
 
 
 # ------------------------------------------------------------- GPU side ---
