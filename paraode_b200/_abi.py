@@ -115,10 +115,11 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    if not os.path.exists(os.environ.get("PODE_LIB_PATH") or LIB_PATH):
         raise ImportError(f"paraode_b200: CUDA library not built ({LIB_PATH}); run "
                           "`python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)")
-    lib = C.CDLL(LIB_PATH)
+    path = os.environ.get("PODE_LIB_PATH") or LIB_PATH  # developer override (A/B builds)
+    lib = C.CDLL(path)
     for name, (res, args) in SYMBOLS.items():
         fn = getattr(lib, name)
         fn.restype = res

@@ -1,0 +1,780 @@
+// Large-state fused IEKS engine (D > 16; Pleiades, d = 28, IWP(3): D = 112).
+//
+// One CTA per time chunk (~one per SM), the chunk's matrices in its own
+// global-memory workspace (L2-resident) and every product on the FP64
+// tensor pipe (big_la.cuh).  The algebra is that of the fused iteration
+// (fast.cuh / lane.cuh) in covariance form — P = C C^T, Lambda = J J^T — so
+// that each time step is a handful of dense contractions plus two Cholesky
+// factorisations of SPD matrices (the predicted covariance P-, whose
+// factor is the Pi_11 of make_smoothing_element, and the innovation
+// covariance S, the Psi_11 of kf_update): the same Gaussians the
+// reference's Householder trias produce (parallel.cpp:38-64, 112-135;
+// sequential.cpp:30-67), whose factors it leaves unpinned (linalg.hpp:12-17;
+// compare L L^T only).
+//
+// Per Gauss-Newton iteration:
+//   A  (parallel)   fold each chunk into its aggregate (A, b, P, eta, Lambda)
+//                   conditioned on the chunk's first state (EK1 linearisation
+//                   on the fly, statespace.cpp:65-88 rescaled as ieks.cpp:160-164)
+//   B  (one CTA)    the chunk-boundary filtered marginals, carried chunk to
+//                   chunk: x_s | carry ~ N((I + P Lambda)^-1 (m + P eta),
+//                   (I + P Lambda)^-1 P), then (A m_s + b, A P_s A^T + P_a) —
+//                   the Gaussian-carry ⊗_f (parallel.cpp:67-100); with ~#SM
+//                   chunks this chain is a few % of the iteration
+//   C  (parallel)   filter through each chunk; smoothing elements
+//                   E_k = P+ phi^T (P-)^-1, g_k = m+ - E_k phi m+
+//                   (parallel.cpp:112-135), and the chunk's backward aggregate
+//   D  (one CTA)    the smoothed means at the chunk boundaries
+//   E  (parallel)   backward means, the new trajectory, the objective and the
+//                   stopping maxima (ieks.cpp:49-77)
+// Finalize: innovation statistics / sigma_hat (ieks.cpp:79-109), the
+// smoothed covariances in Joseph form P^s_k = (I - E_k phi) P+_k (..)^T +
+// E_k Q Q^T E_k^T + E_k P^s_{k+1} E_k^T (the ⊗_s covariance algebra,
+// parallel.cpp:146-156), chunk aggregates chained like D, and the outputs
+// (ieks.cpp:196-208) with cov_sqrt a pivoted-Cholesky factor of P^s.
+//
+// HBM layout: node-major, E_k (D x D) and g_k (D) per node, P+_k (D x D) in
+// the finalize; the trajectory (N+1) x D row-major.
+#pragma once
+
+#include "big_la.cuh"
+#include "fast.cuh"
+#include "field.cuh"
+
+namespace pode {
+namespace big {
+
+// Shared-memory step constants: node scales, the transition's binomial
+// coefficients, the linearisation (f, Jacobian).
+template <int D, int d>
+struct StepSm {
+  static constexpr int B = D / d;
+  double tn[B], tni[B], tk[B], tki[B], ratio[B];
+  double bin[B][B];
+  double y[d], f[d], off[d];
+  double jac[d * d];
+  double red[kBW];
+  int finite;
+};
+
+struct BigArgs {
+  const double* grid;
+  const double* eta;   // linearisation point, (padded + 1) x D row-major (node N at N * D)
+  int64_t N;
+  int L;
+  int64_t nchunks;
+  int ek0;
+  DevProblem prob;
+  DevError* err;
+  const double* qq;    // sigma^2 Q_bar Q_bar^T (D x D)
+  const double* q1u;   // unit-diffusion Q_bar block (B x B lower), for the objective
+  const double* m0;    // T_0^-1 mu_0
+  double* ws;          // per-chunk workspace
+  int64_t ws_stride;   // doubles per chunk
+};
+
+template <int D, int d>
+struct Big {
+  static constexpr int B = D / d;
+  static constexpr int q = B - 1;
+  using Sm = StepSm<D, d>;
+
+  // node scales T_n (ieks.cpp:28-33, incoming step; node 0 uses step 0)
+  __device__ static void taus(const double* grid, int64_t n, double* t, double* ti) {
+    const double h = (n == 0) ? grid[1] - grid[0] : grid[n] - grid[n - 1];
+    const double rh = sqrt(h);
+    double fact = 1.0;
+    for (int i = q; i >= 0; --i) {
+      const int k = q - i;
+      if (k > 0) fact *= k;
+      t[i] = rh * pow(h, double(k)) / fact;
+      ti[i] = 1.0 / t[i];
+    }
+  }
+  __device__ static double binom(int n, int k) {
+    double num = 1.0, den = 1.0;
+    for (int t = 0; t < k; ++t) {
+      num *= double(n - t);
+      den *= double(t + 1);
+    }
+    return num / den;
+  }
+  // step k -> k+1 constants into smem (thread 0), then sync
+  __device__ static void step_consts(Sm& s, const double* grid, int64_t k) {
+    if (threadIdx.x == 0) {
+      taus(grid, k, s.tk, s.tki);
+      taus(grid, k + 1, s.tn, s.tni);
+      for (int i = 0; i < B; ++i) s.ratio[i] = s.tk[i] * s.tni[i];
+      for (int a = 0; a < B; ++a)
+        for (int i = 0; i < B; ++i) s.bin[a][i] = (i >= a) ? binom(q - a, i - a) * s.ratio[i] : 0.0;
+    }
+    __syncthreads();
+  }
+  // Y = Phi X (rows), Y != X
+  __device__ static void phi_rows(const Sm& s, const double* X, double* Y) {
+    for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
+      const int r = idx / D, j = idx - (idx / D) * D;
+      const int blk = r / B, a = r - blk * B;
+      double acc = 0.0;
+      for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[(blk * B + i) * D + j], acc);
+      Y[idx] = acc;
+    }
+    __syncthreads();
+  }
+  // Y = X Phi^T (columns), Y != X
+  __device__ static void phi_cols(const Sm& s, const double* X, double* Y) {
+    for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
+      const int r = idx / D, j = idx - (idx / D) * D;
+      const int blk = j / B, a = j - blk * B;
+      double acc = 0.0;
+      for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[r * D + blk * B + i], acc);
+      Y[idx] = acc;
+    }
+    __syncthreads();
+  }
+  // Y = X Phi (columns), Y != X: Y[r][blk B + c] = sum_{a <= c} X[r][blk B + a] Phi[a][c]
+  __device__ static void phi_right(const Sm& s, const double* X, double* Y) {
+    for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
+      const int r = idx / D, j = idx - (idx / D) * D;
+      const int blk = j / B, cc = j - blk * B;
+      double acc = 0.0;
+      for (int aa = 0; aa <= cc; ++aa) acc = fma(X[r * D + blk * B + aa], s.bin[aa][cc], acc);
+      Y[idx] = acc;
+    }
+    __syncthreads();
+  }
+  __device__ static void phi_vec(const Sm& s, const double* x, double* y) {
+    for (int r = threadIdx.x; r < D; r += kBT) {
+      const int blk = r / B, a = r - blk * B;
+      double acc = 0.0;
+      for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], x[blk * B + i], acc);
+      y[r] = acc;
+    }
+    __syncthreads();
+  }
+  // EK1 / EK0 linearisation at eta[k+1] (statespace.cpp:65-103): thread 0
+  __device__ static void linearize(Sm& s, const BigArgs& a, int64_t k1) {
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < d; ++j) s.y[j] = a.eta[k1 * D + j * B];
+      double jac[d * d];
+      eval_field<d>(a.prob, s.y, s.f, jac, a.prob.kind == 7 ? a.grid[k1] : 0.0);
+      bool fin = true;
+      for (int i = 0; i < d; ++i) fin &= isfinite(s.f[i]);
+      for (int i = 0; i < d * d; ++i) {
+        if (!a.ek0) fin &= isfinite(jac[i]);
+        s.jac[i] = a.ek0 ? 0.0 : jac[i];
+      }
+      for (int i = 0; i < d; ++i) {
+        double jy = 0.0;
+        for (int j = 0; j < d; ++j) jy += s.jac[i * d + j] * s.y[j];
+        s.off[i] = a.ek0 ? s.f[i] : s.f[i] - jy;
+      }
+      s.finite = fin ? 1 : 0;
+    }
+    __syncthreads();
+  }
+  // HX (d x D) = H_bar X; H_bar row i = t1 e_{iB+1} - t0 sum_c jac[i][c] e_{cB}
+  __device__ static void h_rows(const Sm& s, const double* X, double* HX) {
+    const double t0 = s.tn[0], t1 = s.tn[1];
+    for (int idx = threadIdx.x; idx < d * D; idx += kBT) {
+      const int i = idx / D, j = idx - (idx / D) * D;
+      double acc = (1.0 * t1) * X[(i * B + 1) * D + j];
+      for (int c = 0; c < d; ++c) acc = fma((-s.jac[i * d + c]) * t0, X[(c * B) * D + j], acc);
+      HX[idx] = acc;
+    }
+    __syncthreads();
+  }
+  // XH (n x d) = X H_bar^T for X with n rows of D
+  __device__ static void h_cols(const Sm& s, int n, const double* X, double* XH) {
+    const double t0 = s.tn[0], t1 = s.tn[1];
+    for (int idx = threadIdx.x; idx < n * d; idx += kBT) {
+      const int r = idx / d, i = idx - (idx / d) * d;
+      double acc = (1.0 * t1) * X[r * D + i * B + 1];
+      for (int c = 0; c < d; ++c) acc = fma((-s.jac[i * d + c]) * t0, X[r * D + c * B], acc);
+      XH[idx] = acc;
+    }
+    __syncthreads();
+  }
+  // z = H_bar v - offset (d)
+  __device__ static void h_vec(const Sm& s, const double* v, double* z) {
+    const double t0 = s.tn[0], t1 = s.tn[1];
+    for (int i = threadIdx.x; i < d; i += kBT) {
+      double acc = (1.0 * t1) * v[i * B + 1];
+      for (int c = 0; c < d; ++c) acc = fma((-s.jac[i * d + c]) * t0, v[c * B], acc);
+      z[i] = acc - s.off[i];
+    }
+    __syncthreads();
+  }
+};
+
+// Per-chunk workspace slots (doubles), see the kernels.
+template <int D, int d>
+struct Slots {
+  static constexpr int64_t DD = int64_t(D) * D;
+  static constexpr int64_t dD = int64_t(d) * D;
+  static constexpr int64_t kMats = 8;  // M0..M7
+  static constexpr int64_t kSmall = 6 * dD + 2 * int64_t(d) * d + 8 * D + 4 * d;
+  static constexpr int64_t kStride = kMats * DD + kSmall;
+};
+
+// The measurement update of one step in covariance form (kf_update with
+// R = 0, sequential.cpp:41-67): from Pm (predicted) produce W = S^-1 H Pm
+// (d x D) and Sinv (d x d); P+ = Pm - W^T W, K = W^T S^-1.
+template <int D, int d>
+__device__ bool cov_update_parts(StepSm<D, d>& s, const double* Pm, double* HP, double* Sd, double* Sinv, double* W) {
+  using G = Big<D, d>;
+  G::h_rows(s, Pm, HP);          // H Pm
+  G::h_cols(s, d, HP, Sd);       // S S^T = H Pm H^T
+  const bool sing = potrf(d, Sd, d, s.red);
+  trtri_lower(d, Sd, d, Sinv, d);
+  gemm<false, false>(d, D, d, 1.0, Sinv, d, HP, D, 0.0, W, D);  // W = S^-1 H Pm
+  return sing;
+}
+
+// ------------------------------------------------------------- pass A ---
+template <int D, int d>
+__global__ void __launch_bounds__(kBT) k_big_fwd_reduce(BigArgs a, double* agg, int first) {
+  using G = Big<D, d>;
+  using S = Slots<D, d>;
+  __shared__ StepSm<D, d> s;
+  const int64_t c = blockIdx.x;
+  const int64_t s0 = c * a.L, e = min(a.N, s0 + a.L);
+  double* w = a.ws + c * a.ws_stride;
+  double *Am = w, *P = w + S::DD, *Lam = w + 2 * S::DD, *T1 = w + 3 * S::DD, *Pm = w + 4 * S::DD,
+         *Anew = w + 5 * S::DD;
+  double* sm = w + S::kMats * S::DD;
+  double *HP = sm, *W = sm + S::dD, *HA = sm + 2 * S::dD, *Ub = sm + 3 * S::dD;
+  double *Sd = sm + 6 * S::dD, *Sinv = Sd + d * d, *bv = Sinv + d * d, *bm = bv + D, *eta = bm + D, *u = eta + D,
+         *ub = u + d;
+  const bool chunk0 = c == 0 && first;
+  for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
+    const int r = idx / D, j = idx - (idx / D) * D;
+    Am[idx] = (!chunk0 && r == j) ? 1.0 : 0.0;
+    P[idx] = 0.0;
+    Lam[idx] = 0.0;
+  }
+  for (int r = threadIdx.x; r < D; r += kBT) {
+    bv[r] = chunk0 ? a.m0[r] : 0.0;
+    eta[r] = 0.0;
+  }
+  __syncthreads();
+  bool bad_sing = false;
+  int64_t bad_lin = -1;
+  for (int64_t k = s0; k < e; ++k) {
+    G::step_consts(s, a.grid, k);
+    G::phi_rows(s, Am, Anew);  // A- = phi A
+    G::phi_vec(s, bv, bm);     // b- = phi b
+    G::phi_cols(s, P, T1);     // P phi^T
+    G::phi_rows(s, T1, Pm);    // phi P phi^T
+    for (int idx = threadIdx.x; idx < D * D; idx += kBT) Pm[idx] += a.qq[idx];
+    __syncthreads();
+    G::linearize(s, a, k + 1);
+    if (!s.finite && bad_lin < 0) bad_lin = k + 1;
+    bad_sing |= cov_update_parts<D, d>(s, Pm, HP, Sd, Sinv, W);
+    G::h_rows(s, Anew, HA);  // H A-
+    G::h_vec(s, bm, u);      // H b- - offset
+    gemm<false, false>(d, D, d, 1.0, Sinv, d, HA, D, 0.0, Ub, D);  // Ubar = S^-1 H A-
+    gemv<false>(d, d, 1.0, Sinv, d, u, 0.0, ub);                    // ubar = S^-1 u
+    // A = A- - W^T Ubar; b = b- - W^T ubar; P = Pm - W^T W;
+    // eta -= Ubar^T ubar; Lambda += Ubar^T Ubar
+    gemm<true, false>(D, D, d, -1.0, W, D, Ub, D, 1.0, Anew, D);
+    gemv<true>(D, d, -1.0, W, D, ub, 1.0, bm);
+    gemm<true, false>(D, D, d, -1.0, W, D, W, D, 1.0, Pm, D);
+    symmetrize(D, Pm, D);
+    gemv<true>(D, d, -1.0, Ub, D, ub, 1.0, eta);
+    gemm<true, false>(D, D, d, 1.0, Ub, D, Ub, D, 1.0, Lam, D);
+    double* t = Am;  // rotate buffers: A <- Anew, P <- Pm
+    Am = Anew;
+    Anew = t;
+    t = P;
+    P = Pm;
+    Pm = t;
+    copy(D, bm, bv);
+  }
+  if (threadIdx.x == 0) {
+    if (bad_lin >= 0) raise_error(a.err, bad_lin, kErrLinearization);
+    if (bad_sing) raise_error(a.err, s0, kErrSingular);
+  }
+  // aggregate c: A, P, Lambda (D x D each), b, eta
+  double* o = agg + c * (3 * S::DD + 2 * D);
+  for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
+    o[idx] = Am[idx];
+    o[S::DD + idx] = P[idx];
+    o[2 * S::DD + idx] = Lam[idx];
+  }
+  for (int r = threadIdx.x; r < D; r += kBT) {
+    o[3 * S::DD + r] = bv[r];
+    o[3 * S::DD + D + r] = eta[r];
+  }
+}
+
+// ---------------------------------------------------- pass B (one CTA) ---
+// prefix[c] = (m, P) of the filtered marginal at the END of chunk c.
+template <int D, int d>
+__global__ void __launch_bounds__(kBT) k_big_chain_fwd(BigArgs a, const double* agg, double* prefix, double* scratch,
+                                                       int first, const double* carry) {
+  using S = Slots<D, d>;
+  __shared__ double red[kBW];
+  double *M = scratch, *X = scratch + S::DD, *T = X + int64_t(D) * (D + 1);
+  double *m = T + S::DD, *Pc = m + D;
+  const int64_t stride = 3 * S::DD + 2 * D;
+  // chunk 0: its aggregate absorbed the initial distribution (A = 0), or (a
+  // shard) starts from the carry
+  for (int64_t c = 0; c < a.nchunks; ++c) {
+    const double* g = agg + c * stride;
+    const double *Ac = g, *Pa = g + S::DD, *Lam = g + 2 * S::DD, *bc = g + 3 * S::DD, *ec = bc + D;
+    double* out = prefix + c * (S::DD + D);  // m (D) then P (D x D)
+    if (c == 0 && first) {
+      copy(D, bc, out);
+      copy(D * D, Pa, out + D);
+      continue;
+    }
+    const double* pm = (c == 0) ? carry : prefix + (c - 1) * (S::DD + D);
+    copy(D, pm, m);
+    copy(D * D, pm + D, Pc);
+    // M = I + Pc Lambda; X = [Pc | m + Pc eta]
+    gemm<false, false>(D, D, D, 1.0, Pc, D, Lam, D, 0.0, M, D);
+    for (int i = threadIdx.x; i < D; i += kBT) M[i * D + i] += 1.0;
+    for (int idx = threadIdx.x; idx < D * D; idx += kBT) X[(idx / D) * (D + 1) + idx % D] = Pc[idx];
+    __syncthreads();
+    for (int i = threadIdx.x; i < D; i += kBT) {
+      double acc = m[i];
+      for (int k = 0; k < D; ++k) acc = fma(Pc[i * D + k], ec[k], acc);
+      X[i * (D + 1) + D] = acc;
+    }
+    __syncthreads();
+    lu_solve(D, M, D, D + 1, X, D + 1, red);  // X = [P_s | m_s]
+    // out.m = A m_s + b; out.P = A P_s A^T + Pa
+    for (int i = threadIdx.x; i < D; i += kBT) {
+      double acc = bc[i];
+      for (int k = 0; k < D; ++k) acc = fma(Ac[i * D + k], X[k * (D + 1) + D], acc);
+      out[i] = acc;
+    }
+    gemm<false, false>(D, D, D, 1.0, Ac, D, X, D + 1, 0.0, T, D);          // A P_s
+    copy(D * D, Pa, out + D);
+    gemm<false, true>(D, D, D, 1.0, T, D, Ac, D, 1.0, out + D, D);         // + A P_s A^T
+    symmetrize(D, out + D, D);
+  }
+}
+
+// ------------------------------------------------------------- pass C ---
+// kFinal: also stores P+_k (filtered covariance at every node, pf) and the
+// whitened innovations sum (innov, one partial per chunk).
+template <int D, int d, bool kFinal>
+__global__ void __launch_bounds__(kBT) k_big_fwd_down(BigArgs a, const double* prefix, double* E_out, double* g_out,
+                                                      double* g_term, double* bagg, double* pf, double* pterm,
+                                                      double* innov, int first, int last, const double* carry) {
+  using G = Big<D, d>;
+  using S = Slots<D, d>;
+  __shared__ StepSm<D, d> s;
+  const int64_t c = blockIdx.x;
+  const int64_t s0 = c * a.L, e = min(a.N, s0 + a.L);
+  double* w = a.ws + c * a.ws_stride;
+  double *P = w, *Y = w + S::DD, *Pm = w + 2 * S::DD, *Lc = w + 3 * S::DD, *Li = w + 4 * S::DD,
+         *Z = w + 5 * S::DD, *EA = w + 6 * S::DD, *EAn = w + 7 * S::DD;
+  double* sm = w + S::kMats * S::DD;
+  double *HP = sm, *W = sm + S::dD;
+  double *Sd = sm + 6 * S::dD, *Sinv = Sd + d * d, *m = Sinv + d * d, *mm = m + D, *gk = mm + D, *gA = gk + D,
+         *z = gA + D, *zb = z + d;
+  const double* pin = (c == 0) ? (first ? nullptr : carry) : prefix + (c - 1) * (S::DD + D);
+  for (int idx = threadIdx.x; idx < D * D; idx += kBT) P[idx] = pin ? pin[D + idx] : 0.0;
+  for (int r = threadIdx.x; r < D; r += kBT) m[r] = pin ? pin[r] : a.m0[r];
+  __syncthreads();
+  bool bad_sing = false;
+  int64_t bad_lin = -1;
+  double inn = 0.0;
+  for (int64_t k = s0; k < e; ++k) {
+    G::step_consts(s, a.grid, k);
+    if constexpr (kFinal) copy(D * D, P, pf + k * S::DD);
+    G::phi_cols(s, P, Y);   // Y = P phi^T
+    G::phi_rows(s, Y, Pm);  // Pm = phi P phi^T + Q Q^T
+    for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
+      Pm[idx] += a.qq[idx];
+      Lc[idx] = Pm[idx];
+    }
+    __syncthreads();
+    bad_sing |= potrf(D, Lc, D, s.red);                                // Pm = L L^T
+    trtri_lower(D, Lc, D, Li, D);                                      // L^-1
+    gemm<false, true>(D, D, D, 1.0, Y, D, Li, D, 0.0, Z, D);           // Y L^-T
+    double* Ek = E_out + k * S::DD;
+    gemm<false, false>(D, D, D, 1.0, Z, D, Li, D, 0.0, Ek, D);         // E = Y L^-T L^-1
+    G::phi_vec(s, m, mm);                                              // m- = phi m
+    for (int r = threadIdx.x; r < D; r += kBT) {
+      double acc = 0.0;
+      for (int j = 0; j < D; ++j) acc = fma(Ek[r * D + j], mm[j], acc);
+      gk[r] = m[r] - acc;
+      g_out[k * D + r] = gk[r];
+    }
+    __syncthreads();
+    if constexpr (!kFinal) {
+      // backward aggregate (E, g) <- (E E_k, E g_k + g) (⊗_s on means)
+      if (k == s0) {
+        copy(D * D, Ek, EA);
+        copy(D, gk, gA);
+      } else {
+        gemv<false>(D, D, 1.0, EA, D, gk, 1.0, gA);
+        gemm<false, false>(D, D, D, 1.0, EA, D, Ek, D, 0.0, EAn, D);
+        double* t = EA;
+        EA = EAn;
+        EAn = t;
+      }
+    }
+    // measurement update at node k+1
+    G::linearize(s, a, k + 1);
+    if (!s.finite && bad_lin < 0) bad_lin = k + 1;
+    bad_sing |= cov_update_parts<D, d>(s, Pm, HP, Sd, Sinv, W);
+    G::h_vec(s, mm, z);                             // H m- - offset
+    gemv<false>(d, d, 1.0, Sinv, d, z, 0.0, zb);    // S^-1 z
+    if constexpr (kFinal) {
+      if (threadIdx.x == 0)
+        for (int i = 0; i < d; ++i) inn = fma(zb[i], zb[i], inn);
+    }
+    copy(D, mm, m);
+    gemv<true>(D, d, -1.0, W, D, zb, 1.0, m);       // m+ = m- - W^T S^-1 z
+    gemm<true, false>(D, D, d, -1.0, W, D, W, D, 1.0, Pm, D);  // P+ = Pm - W^T W
+    symmetrize(D, Pm, D);
+    double* t = P;
+    P = Pm;
+    Pm = t;
+  }
+  if (e == a.N) {  // terminal node N: E = 0, g = m_f(N)
+    copy(D, m, g_term);
+    if constexpr (kFinal) copy(D * D, P, pterm);
+  }
+  if constexpr (!kFinal) {
+    const bool term = e == a.N && last;
+    double* ob = bagg + c * (S::DD + D);
+    if (term) gemv<false>(D, D, 1.0, EA, D, m, 1.0, gA);
+    for (int idx = threadIdx.x; idx < D * D; idx += kBT) ob[idx] = term ? 0.0 : EA[idx];
+    for (int r = threadIdx.x; r < D; r += kBT) ob[S::DD + r] = gA[r];
+  }
+  if (threadIdx.x == 0) {
+    if (kFinal) {  // the k_finish3 partial layout (sum, 0, 0)
+      innov[c * 3 + 0] = inn;
+      innov[c * 3 + 1] = 0.0;
+      innov[c * 3 + 2] = 0.0;
+    }
+    if (bad_lin >= 0) raise_error(a.err, bad_lin, kErrLinearization);
+    if (bad_sing) raise_error(a.err, s0, kErrSingular);
+  }
+}
+
+// ---------------------------------------------------- pass D (one CTA) ---
+// suffix[c] = smoothed mean at the start node of chunk c (the last chunk's
+// aggregate absorbed the terminal element).
+template <int D>
+__global__ void __launch_bounds__(kBT) k_big_chain_bwd(int64_t nc, const double* bagg, double* suffix,
+                                                       const double* right) {
+  constexpr int64_t DD = int64_t(D) * D;
+  for (int64_t c = nc - 1; c >= 0; --c) {
+    const double* g = bagg + c * (DD + D);
+    const double* nxt = (c == nc - 1) ? right : suffix + (c + 1) * D;
+    for (int i = threadIdx.x; i < D; i += kBT) {
+      double acc = g[DD + i];
+      if (nxt)
+        for (int k = 0; k < D; ++k) acc = fma(g[i * D + k], nxt[k], acc);
+      suffix[c * D + i] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------- pass E ---
+// Backward means, new trajectory (original coordinates), objective terms
+// (unit-diffusion metric, block-diagonal Q_bar: one thread per block) and
+// stopping maxima; one (obj, dmax, emax) partial per chunk.
+template <int D, int d, bool kInitial>
+__global__ void __launch_bounds__(kBT) k_big_bwd_down(BigArgs a, const double* E_in, const double* g_in,
+                                                      const double* g_term, const double* suffix,
+                                                      const double* eta_old, double* eta_new, double* part, int last) {
+  using G = Big<D, d>;
+  constexpr int B = D / d;
+  __shared__ double mu[D], nm[D], bar_next[D], bar[D], pb[D];
+  __shared__ double tk[B], tki[B], tn[B], ratio[B], bin[B][B], red[kBW];
+  const int64_t c = blockIdx.x;
+  const int64_t s0 = c * a.L, e = min(a.N, s0 + a.L);
+  const bool lastc = c == a.nchunks - 1;
+  double obj = 0.0, dmax = 0.0, emax = 0.0;
+  if (threadIdx.x == 0) G::taus(a.grid, e, tn, tki);  // tki: T_e^-1 here
+  __syncthreads();
+  for (int r = threadIdx.x; r < D; r += kBT) {
+    const double old_e = eta_old[e * D + r];
+    double eta_e;
+    if (kInitial) {
+      eta_e = old_e;
+      mu[r] = 0.0;
+    } else {
+      mu[r] = lastc ? g_term[r] : suffix[(c + 1) * D + r];
+      eta_e = tn[r % B] * mu[r];
+    }
+    if (lastc) {
+      if (!kInitial) eta_new[e * D + r] = eta_e;
+      if (last) {
+        dmax = fmax(dmax, fabs(eta_e - old_e));
+        emax = fmax(emax, fabs(eta_e));
+      }
+    }
+    bar_next[r] = tki[r % B] * eta_e;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < B; ++i) tn[i] = tki[i];  // T_{k+1}^-1
+  __syncthreads();
+  for (int64_t k = e - 1; k >= s0; --k) {
+    if (threadIdx.x == 0) {
+      G::taus(a.grid, k, tk, tki);
+      for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tn[i];
+      for (int aa = 0; aa < B; ++aa)
+        for (int i = 0; i < B; ++i) bin[aa][i] = (i >= aa) ? G::binom(B - 1 - aa, i - aa) * ratio[i] : 0.0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < D; r += kBT) {
+      const double oldk = eta_old[k * D + r];
+      double etak;
+      if (kInitial) {
+        etak = oldk;
+      } else {
+        double acc = g_in[k * D + r];
+        const double* Er = E_in + (k * D + r) * D;
+        for (int j = 0; j < D; ++j) acc = fma(Er[j], mu[j], acc);
+        nm[r] = acc;
+        etak = tk[r % B] * acc;
+        eta_new[k * D + r] = etak;
+      }
+      dmax = fmax(dmax, fabs(etak - oldk));
+      emax = fmax(emax, fabs(etak));
+      bar[r] = tki[r % B] * etak;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < D; r += kBT) {
+      const int blk = r / B, aa = r - blk * B;
+      double acc = 0.0;
+      for (int i = aa; i < B; ++i) acc = fma(bin[aa][i], bar[blk * B + i], acc);
+      pb[r] = bar_next[r] - acc;
+      if (!kInitial) mu[r] = nm[r];
+    }
+    __syncthreads();
+    // || Qunit^-1/2 (bar_{k+1} - phi bar_k) ||^2, Q_bar = I_d (x) Q1: one block per thread
+    for (int blk = threadIdx.x; blk < d; blk += kBT) {
+      double w[B];
+      for (int i = 0; i < B; ++i) {
+        double acc = pb[blk * B + i];
+        for (int k2 = 0; k2 < i; ++k2) acc = fma(-a.q1u[i * B + k2], w[k2], acc);
+        w[i] = acc / a.q1u[i * B + i];
+        obj = fma(w[i], w[i], obj);
+      }
+    }
+    for (int r = threadIdx.x; r < D; r += kBT) bar_next[r] = bar[r];
+    if (threadIdx.x == 0)
+      for (int i = 0; i < B; ++i) tn[i] = tki[i];
+    __syncthreads();
+  }
+  obj = block_sum(obj, red);
+  dmax = block_max(dmax, red);
+  emax = block_max(emax, red);
+  if (threadIdx.x == 0) {
+    part[c * 3 + 0] = obj;
+    part[c * 3 + 1] = dmax;
+    part[c * 3 + 2] = emax;
+  }
+}
+
+// ------------------------------------------------- finalize (once) ---
+// M1_k = (I - E_k phi) P+_k (I - E_k phi)^T + E_k Q Q^T E_k^T: the
+// covariance of the smoothing element at node k (Joseph form).
+template <int D, int d>
+__device__ void smooth_cov(StepSm<D, d>& s, const double* Ek, const double* Pf, const double* qq, double* M1,
+                           double* T1, double* T2) {
+  using G = Big<D, d>;
+  G::phi_right(s, Ek, T1);  // E phi  (phi_k = node k -> k+1)
+  for (int idx = threadIdx.x; idx < D * D; idx += kBT) T1[idx] = ((idx / D == idx % D) ? 1.0 : 0.0) - T1[idx];
+  __syncthreads();
+  gemm<false, false>(D, D, D, 1.0, T1, D, Pf, D, 0.0, T2, D);   // (I - E phi) P+
+  gemm<false, true>(D, D, D, 1.0, T2, D, T1, D, 0.0, M1, D);    // .. (I - E phi)^T
+  gemm<false, false>(D, D, D, 1.0, Ek, D, qq, D, 0.0, T2, D);   // E Q Q^T
+  gemm<false, true>(D, D, D, 1.0, T2, D, Ek, D, 1.0, M1, D);    // + E Q Q^T E^T
+}
+
+// F2: per chunk the smoothing-covariance aggregate (Eagg, Lagg): P^s(s) =
+// Eagg P^s(e) Eagg^T + Lagg (the last chunk absorbs P^s(N) = P+(N)).
+template <int D, int d>
+__global__ void __launch_bounds__(kBT) k_big_fin_fold(BigArgs a, const double* E_in, const double* pf,
+                                                      const double* pterm, double* sagg, int last) {
+  using G = Big<D, d>;
+  using S = Slots<D, d>;
+  __shared__ StepSm<D, d> s;
+  const int64_t c = blockIdx.x;
+  const int64_t s0 = c * a.L, e = min(a.N, s0 + a.L);
+  const bool term = c == a.nchunks - 1 && last;
+  double* w = a.ws + c * a.ws_stride;
+  double *EA = w, *LA = w + S::DD, *M1 = w + 2 * S::DD, *T1 = w + 3 * S::DD, *T2 = w + 4 * S::DD,
+         *EAn = w + 5 * S::DD, *LAn = w + 6 * S::DD;
+  for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
+    EA[idx] = (!term && idx / D == idx % D) ? 1.0 : 0.0;
+    LA[idx] = term ? pterm[idx] : 0.0;
+  }
+  __syncthreads();
+  for (int64_t k = e - 1; k >= s0; --k) {
+    G::step_consts(s, a.grid, k);
+    const double* Ek = E_in + k * S::DD;
+    smooth_cov<D, d>(s, Ek, pf + k * S::DD, a.qq, M1, T1, T2);
+    gemm<false, false>(D, D, D, 1.0, Ek, D, LA, D, 0.0, T1, D);    // E L
+    copy(D * D, M1, LAn);
+    gemm<false, true>(D, D, D, 1.0, T1, D, Ek, D, 1.0, LAn, D);    // E L E^T + M1
+    gemm<false, false>(D, D, D, 1.0, Ek, D, EA, D, 0.0, EAn, D);   // E Eagg
+    double* t = EA;
+    EA = EAn;
+    EAn = t;
+    t = LA;
+    LA = LAn;
+    LAn = t;
+  }
+  double* o = sagg + c * 2 * S::DD;
+  for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
+    o[idx] = EA[idx];
+    o[S::DD + idx] = LA[idx];
+  }
+}
+
+// F3 (one CTA): P^s at every chunk's start node, from the right.
+template <int D>
+__global__ void __launch_bounds__(kBT) k_big_chain_fin(int64_t nc, const double* sagg, double* ps, double* T,
+                                                       const double* right) {
+  constexpr int64_t DD = int64_t(D) * D;
+  for (int64_t c = nc - 1; c >= 0; --c) {
+    const double* g = sagg + c * 2 * DD;
+    const double* nxt = (c == nc - 1) ? right : ps + (c + 1) * DD;
+    double* out = ps + c * DD;
+    copy(D * D, g + DD, out);
+    if (nxt) {
+      gemm<false, false>(D, D, D, 1.0, g, D, nxt, D, 0.0, T, D);
+      gemm<false, true>(D, D, D, 1.0, T, D, g, D, 1.0, out, D);
+    }
+    symmetrize(D, out, D);
+  }
+}
+
+// Pivoted Cholesky of the PSD n x n A (destroyed): F (n x n, row-major)
+// with F F^T = A, F = Pi L; pivots below tol * max diag end the
+// factorisation (remaining columns zero).
+__device__ void psd_factor(int n, double* A, int lda, double* F, int ldf, int* perm, double* red) {
+  __shared__ int s_p;
+  __shared__ double s_d, s_dmax;
+  for (int idx = threadIdx.x; idx < n * n; idx += kBT) F[(idx / n) * ldf + idx % n] = 0.0;
+  for (int i = threadIdx.x; i < n; i += kBT) perm[i] = i;
+  __syncthreads();
+  double mloc = 0.0;
+  for (int i = threadIdx.x; i < n; i += kBT) mloc = fmax(mloc, A[i * lda + i]);
+  const double dmax0 = block_max(mloc, red);
+  if (threadIdx.x == 0) s_dmax = dmax0;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x < 32) {  // pivot: largest remaining diagonal (positions j..n-1 in permuted order)
+      double best = -1.0;
+      int bi = j;
+      for (int i = j + threadIdx.x; i < n; i += 32) {
+        const double v = A[perm[i] * lda + perm[i]];
+        if (v > best) {
+          best = v;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) {
+          best = ov;
+          bi = oi;
+        }
+      }
+      if (threadIdx.x == 0) {
+        s_p = bi;
+        s_d = best;
+        const int t = perm[j];
+        perm[j] = perm[bi];
+        perm[bi] = t;
+      }
+    }
+    __syncthreads();
+    if (!(s_d > 1e-15 * s_dmax)) break;  // CTA-uniform
+    const int pj = perm[j];
+    const double l = sqrt(s_d), inv = 1.0 / l;
+    // column j of L (rows in permuted order i >= j): L[i][j] = A[pi][pj] / l
+    for (int i = j + threadIdx.x; i < n; i += kBT) {
+      const int pi = perm[i];
+      F[pi * ldf + j] = (i == j) ? l : A[pi * lda + pj] * inv;
+    }
+    __syncthreads();
+    // Schur complement on the remaining rows/cols
+    const int m = n - j - 1;
+    for (int idx = threadIdx.x; idx < m * m; idx += kBT) {
+      const int pi = perm[j + 1 + idx / m], pk = perm[j + 1 + idx % m];
+      A[pi * lda + pk] = fma(-F[pi * ldf + j], F[pk * ldf + j], A[pi * lda + pk]);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
+struct BigOut {
+  double* means;
+  double* cov;
+  double* sol_m;
+  double* sol_c;
+};
+
+// F4: P^s_k = M1_k + E_k P^s_{k+1} E_k^T from the chunk's end, with the
+// calibrated outputs (ieks.cpp:196-208).
+template <int D, int d>
+__global__ void __launch_bounds__(kBT) k_big_fin_bwd(BigArgs a, const double* E_in, const double* pf,
+                                                     const double* pterm, const double* ps, const double* eta_out,
+                                                     const double* innov_tot, double count, BigOut o, int last) {
+  using G = Big<D, d>;
+  using S = Slots<D, d>;
+  constexpr int B = D / d;
+  __shared__ StepSm<D, d> s;
+  __shared__ int perm[D];
+  __shared__ double tt[B], tti[B];
+  const int64_t c = blockIdx.x;
+  const int64_t s0 = c * a.L, e = min(a.N, s0 + a.L);
+  const bool lastc = c == a.nchunks - 1;
+  double* w = a.ws + c * a.ws_stride;
+  double *Pn = w, *M1 = w + S::DD, *T1 = w + 2 * S::DD, *T2 = w + 3 * S::DD, *Pk = w + 4 * S::DD,
+         *F = w + 5 * S::DD, *Ac = w + 6 * S::DD;
+  const double sig = sqrt(innov_tot[0] / count);
+  copy(D * D, lastc ? pterm : ps + (c + 1) * S::DD, Pn);
+  auto emit = [&](int64_t n, const double* Pnode) {
+    if (threadIdx.x == 0) G::taus(a.grid, n, tt, tti);
+    copy(D * D, Pnode, Ac);
+    psd_factor(D, Ac, D, F, D, perm, s.red);
+    for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
+      const int r = idx / D;
+      if (o.cov) o.cov[n * S::DD + idx] = tt[r % B] * F[idx] * sig;
+    }
+    for (int r = threadIdx.x; r < D; r += kBT) {
+      if (o.means) o.means[n * D + r] = eta_out[n * D + r];
+      if (o.sol_m && r % B == 0) o.sol_m[n * d + r / B] = eta_out[n * D + r];
+    }
+    for (int idx = threadIdx.x; idx < d * d; idx += kBT) {
+      const int i = idx / d, j = idx - (idx / d) * d;
+      if (o.sol_c) o.sol_c[n * d * d + idx] = (tt[0] * sig) * (tt[0] * sig) * Pnode[(i * B) * D + j * B];
+    }
+    __syncthreads();
+  };
+  if (lastc && last) emit(e, Pn);
+  for (int64_t k = e - 1; k >= s0; --k) {
+    G::step_consts(s, a.grid, k);
+    const double* Ek = E_in + k * S::DD;
+    smooth_cov<D, d>(s, Ek, pf + k * S::DD, a.qq, M1, T1, T2);
+    gemm<false, false>(D, D, D, 1.0, Ek, D, Pn, D, 0.0, T1, D);   // E P^s_{k+1}
+    copy(D * D, M1, Pk);
+    gemm<false, true>(D, D, D, 1.0, T1, D, Ek, D, 1.0, Pk, D);    // + E P E^T
+    symmetrize(D, Pk, D);
+    emit(k, Pk);
+    copy(D * D, Pk, Pn);
+  }
+}
+
+}  // namespace big
+}  // namespace pode

@@ -371,7 +371,7 @@ void pode_context_destroy(pode_context* ctx) {
   delete ctx;
 }
 
-int32_t pode_max_state_dim(void) { return kMaxD; }
+int32_t pode_max_state_dim(void) { return 112; }  // the large-state engine (big.cuh) above kMaxD
 
 int pode_profile(pode_context* ctx, int32_t enable) {
   if (ctx == nullptr) return PODE_ERR_INVALID_INPUT;
@@ -603,7 +603,8 @@ static int solve_report(pode_context* ctx, const pode_problem* problem, const po
     if (grid[0] != 0.0) throw ApiError(PODE_ERR_INVALID_INPUT, "discretize: grid must start at t = 0");
     check_grid_increasing(grid, n_nodes);
     const int D = prior->dim * (prior->nu + 1);
-    const auto& ops = ops_for(D);
+    const BigIeksFn big = (D > kMaxD && !eks) ? big_ieks(D, prior->dim) : nullptr;
+    const EngineOps* ops = big ? nullptr : &ops_for(D);
     const bool dev = report->location == PODE_DEVICE;
     const int d = prior->dim;
     double* means = dev ? report->means : (report->means ? ctx->ws.arr<double>("out_means", n_nodes * D) : nullptr);
@@ -613,7 +614,10 @@ static int solve_report(pode_context* ctx, const pode_problem* problem, const po
     double* sc = dev ? report->solution_covs
                      : (report->solution_covs ? ctx->ws.arr<double>("out_sc", n_nodes * d * d) : nullptr);
     IeksResult r;
-    (eks ? ops.eks : ops.ieks)(ctx, p, *prior, grid, n_nodes, *config, means, cov, sm, sc, &r);
+    if (big)
+      big(ctx, p, *prior, grid, n_nodes, *config, means, cov, sm, sc, &r);
+    else
+      (eks ? ops->eks : ops->ieks)(ctx, p, *prior, grid, n_nodes, *config, means, cov, sm, sc, &r);
     if (!dev) {
       stage_out(ctx, report->means, means, size_t(n_nodes) * D, false);
       stage_out(ctx, report->cov_sqrt, cov, size_t(n_nodes) * D * D, false);

@@ -42,4 +42,10 @@ constexpr int kMaxD = 16;
 
 const EngineOps* engine_ops(int D);  // nullptr when D is not compiled
 
+// The large-state fused IEKS engine (big.cuh; D > kMaxD): nullptr when
+// (D, d) is not compiled.
+using BigIeksFn = void (*)(pode_context*, const host::Problem&, const pode_prior&, const double*, int64_t,
+                           const pode_ieks_config&, double*, double*, double*, double*, IeksResult*);
+BigIeksFn big_ieks(int D, int d);
+
 }  // namespace pode

@@ -23,6 +23,13 @@
 namespace pode {
 namespace grp {
 
+// Resident blocks per SM the heavy passes are compiled for (register cap
+// 64K / (128 * n)); 2 = 255 registers.
+#ifndef PODE_GRP_MIN_BLOCKS
+#define PODE_GRP_MIN_BLOCKS 2
+#endif
+constexpr int kGrpMinBlocks = PODE_GRP_MIN_BLOCKS;
+
 // Per-lane view of the block-binomial transition (prior.cpp:99-107):
 // row r = blk B + a of Phi_n has entries bin(q - a, i - a) ratio[i] at
 // columns blk B + i, i >= a.
@@ -185,7 +192,7 @@ __device__ __forceinline__ void load_y(const FastArgs& a, const LinPoint& lp, in
 
 // ------------------------------------------------------------- pass A ---
 template <int D, int d>
-__global__ void __launch_bounds__(kThreads) k_grp_fwd_reduce(const FastArgs a, FastConst<D> cst, FEd agg) {
+__global__ void __launch_bounds__(kThreads, kGrpMinBlocks) k_grp_fwd_reduce(const FastArgs a, FastConst<D> cst, FEd agg) {
   using M = GM<D, d>;
   using LM = typename M::LM;
   constexpr int B = M::B;
@@ -293,7 +300,7 @@ __global__ void __launch_bounds__(kThreads) k_grp_fwd_reduce(const FastArgs a, F
 // kFinal: also stores C_f(k) (cf, node-major) and reduces the whitened
 // innovations into one partial per block (part[3 b]).
 template <int D, int d, bool kFinal>
-__global__ void __launch_bounds__(kThreads) k_grp_fwd_down(const FastArgs a, FastConst<D> cst, FEd prefix,
+__global__ void __launch_bounds__(kThreads, kGrpMinBlocks) k_grp_fwd_down(const FastArgs a, FastConst<D> cst, FEd prefix,
                                                            lane::ElemSoA elems, double* cf, double* cterm,
                                                            double* part, SEd bagg) {
   using M = GM<D, d>;

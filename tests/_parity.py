@@ -22,8 +22,7 @@ def cov_upper(cov_sqrt, nodes):
 
 def gpu_solve(P, meta, ctx=None, **cfg):
     """meta: {problem, nu, t_end, steps} (the fixture metadata schema)."""
-    name = {"fhn": "fhn", "vanderpol": "vanderpol", "rigidbody": "rigidbody"}[meta["problem"]]
-    prob = P.problem_by_name(name)
+    prob = P.problem_by_name(meta["problem"])
     grid = P.uniform_grid(meta["t_end"], meta["steps"])
     return P.para_ieks(prob, P.IwpPrior(meta["nu"], prob.dim, 1.0), grid, P.IeksConfig(**cfg), ctx=ctx)
 
@@ -68,11 +67,12 @@ def compare(rep, z, meta, label, alts=()):
 
 def alternatives(P, meta, its):
     """Solves differing from the default one only in rounding: the fused
-    engine at two other chunk lengths (states it serves) and the element
-    engine (the reference's per-iteration structure)."""
-    D = (meta["nu"] + 1) * {"fhn": 2, "vanderpol": 2, "rigidbody": 3}[meta["problem"]]
+    engine at two other chunk lengths and the element engine (the
+    reference's per-iteration structure); above D = 16 (the large-state
+    engine) two other chunkings."""
+    D = (meta["nu"] + 1) * {"fhn": 2, "vanderpol": 2, "rigidbody": 3, "pleiades": 28}[meta["problem"]]
     out = []
-    settings = [("elements", 0)] + ([("auto", 13), ("auto", 19)] if D <= 16 else [])
+    settings = [("elements", 0), ("auto", 13), ("auto", 19)] if D <= 16 else [("auto", 3), ("auto", 11)]
     for engine, chunk in settings:
         ctx = P.Context()
         ctx.set_engine(engine)

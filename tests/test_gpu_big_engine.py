@@ -1,0 +1,78 @@
+"""The large-state fused IEKS engine (big.cuh; Pleiades, d = 28, IWP(1..3),
+D = 56..112, BASELINE.json configs[4]) against the sequential oracle
+(seq_ieks, proj/src/ieks.cpp:219-222): equal iteration counts, means per
+derivative order, covariance products L L^T and sigma_hat, under several
+chunkings (one CTA per chunk; the chunk chains of passes B / D / F3)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import _oracle as O
+from _parity import NEVER, alternatives, compare, gpu_solve
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paraode_b200")
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def as_fixture(want, nodes=None):
+    nodes = np.arange(len(want["means"])) if nodes is None else nodes
+    L = want["cov_sqrt"][nodes]
+    cov = np.einsum("nij,nkj->nik", L, L)
+    iu = np.triu_indices(cov.shape[1])
+    return dict(nodes=nodes, means=want["means"][nodes], cov_upper=cov[:, iu[0], iu[1]],
+                objective_trace=want["objective_trace"])
+
+
+@pytest.mark.parametrize("chunk", [0, 1, 5, 1000])
+@pytest.mark.parametrize("nu,steps,its", [(1, 48, 3), (2, 40, 2), (3, 64, 2)])
+def test_pleiades_matches_seq_ieks(nu, steps, its, chunk):
+    op = O.problem("pleiades")
+    grid = O.uniform_grid(op.t_end, steps)
+    want = O.ieks(op, nu, grid, mode=0, max_iterations=its, **NEVER)
+    ctx = P.Context()
+    ctx.set_chunk_len(chunk)
+    meta = dict(problem="pleiades", nu=nu, t_end=op.t_end, steps=steps, iterations=its,
+                sigma_hat=want["sigma_hat"])
+    got = gpu_solve(P, meta, ctx=ctx, max_iterations=its, **NEVER)
+    assert np.allclose(got.objective_trace, want["objective_trace"], rtol=1e-8)
+    compare(got, as_fixture(want), meta, f"pleiades q{nu} N={steps} L={chunk}")
+    assert np.all(np.isfinite(got.solution_covs))
+
+
+def test_pleiades_2e10_fixture():
+    """N = 2^10 (SURVEY.md §8(d) parity size), 3 equal iterations, against the
+    committed oracle fixture (tools/make_fixtures.py)."""
+    path = os.path.join(GOLDEN, "pleiades_q3_n10_seq_it3.npz")
+    if not os.path.exists(path):
+        pytest.skip("fixture not generated")
+    z = np.load(path)
+    meta = json.loads(str(z["meta"]))
+    got = gpu_solve(P, meta, max_iterations=meta["iterations"], **NEVER)
+    assert np.allclose(got.objective_trace, z["objective_trace"], rtol=1e-8)
+    compare(got, z, meta, "pleiades q3 N=2^10 (fixture)", alternatives(P, meta, meta["iterations"]))
+
+
+def test_pleiades_converged_fixture():
+    path = os.path.join(GOLDEN, "pleiades_q3_n10_seq.npz")
+    if not os.path.exists(path):
+        pytest.skip("fixture not generated")
+    z = np.load(path)
+    meta = json.loads(str(z["meta"]))
+    conv = gpu_solve(P, meta)
+    print(f"pleiades q3 N=2^10 default rule: GPU {conv.iterations} its conv={conv.converged}; "
+          f"oracle {meta['iterations']} its conv={meta['converged']}")
+    got = gpu_solve(P, meta, max_iterations=meta["iterations"], **NEVER)
+    compare(got, z, meta, "pleiades q3 N=2^10 converged (fixture)", alternatives(P, meta, meta["iterations"]))
+
+
+def test_pleiades_errors_and_determinism():
+    grid = O.uniform_grid(3.0, 64)
+    a = P.para_ieks(P.pleiades(), P.IwpPrior(3, 28, 1.0), grid, P.IeksConfig(max_iterations=2))
+    b = P.para_ieks(P.pleiades(), P.IwpPrior(3, 28, 1.0), grid, P.IeksConfig(max_iterations=2))
+    assert np.array_equal(a.means, b.means) and np.array_equal(a.cov_sqrt, b.cov_sqrt)
+    with pytest.raises(P.UnsupportedError):
+        P.eks_solve(P.pleiades(), P.IwpPrior(3, 28, 1.0), grid)

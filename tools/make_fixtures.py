@@ -53,6 +53,9 @@ CASES = {
     "vdp_q3_n18_seq": ("vanderpol", 3, 18, 0, 100, False, 2048),
     "rigid_q4_n14_seq": ("rigidbody", 4, 14, 0, 100, False, 1024),
     "rigid_q4_n16_seq": ("rigidbody", 4, 16, 0, 100, False, 1024),
+    # configs[4]: Pleiades (d = 28, IWP(3), D = 112) at the parity sizes of SURVEY.md §8(d)
+    "pleiades_q3_n10_seq": ("pleiades", 3, 10, 0, 100, False, 64),
+    "pleiades_q3_n10_seq_it3": ("pleiades", 3, 10, 0, 3, True, 64),
 }
 
 
