@@ -112,35 +112,36 @@ struct Big {
   }
   // Y = Phi X (rows), Y != X
   __device__ static void phi_rows(const Sm& s, const double* X, double* Y) {
-    for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
-      const int r = idx / D, j = idx - (idx / D) * D;
+    for (int r = threadIdx.x >> 5; r < D; r += kBW) {
       const int blk = r / B, a = r - blk * B;
-      double acc = 0.0;
-      for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[(blk * B + i) * D + j], acc);
-      Y[idx] = acc;
+      for (int j = threadIdx.x & 31; j < D; j += 32) {
+        double acc = 0.0;
+        for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[(blk * B + i) * D + j], acc);
+        Y[r * D + j] = acc;
+      }
     }
     __syncthreads();
   }
   // Y = X Phi^T (columns), Y != X
   __device__ static void phi_cols(const Sm& s, const double* X, double* Y) {
-    for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
-      const int r = idx / D, j = idx - (idx / D) * D;
-      const int blk = j / B, a = j - blk * B;
-      double acc = 0.0;
-      for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[r * D + blk * B + i], acc);
-      Y[idx] = acc;
-    }
+    for (int r = threadIdx.x >> 5; r < D; r += kBW)
+      for (int j = threadIdx.x & 31; j < D; j += 32) {
+        const int blk = j / B, a = j - blk * B;
+        double acc = 0.0;
+        for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[r * D + blk * B + i], acc);
+        Y[r * D + j] = acc;
+      }
     __syncthreads();
   }
   // Y = X Phi (columns), Y != X: Y[r][blk B + c] = sum_{a <= c} X[r][blk B + a] Phi[a][c]
   __device__ static void phi_right(const Sm& s, const double* X, double* Y) {
-    for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
-      const int r = idx / D, j = idx - (idx / D) * D;
-      const int blk = j / B, cc = j - blk * B;
-      double acc = 0.0;
-      for (int aa = 0; aa <= cc; ++aa) acc = fma(X[r * D + blk * B + aa], s.bin[aa][cc], acc);
-      Y[idx] = acc;
-    }
+    for (int r = threadIdx.x >> 5; r < D; r += kBW)
+      for (int j = threadIdx.x & 31; j < D; j += 32) {
+        const int blk = j / B, cc = j - blk * B;
+        double acc = 0.0;
+        for (int aa = 0; aa <= cc; ++aa) acc = fma(X[r * D + blk * B + aa], s.bin[aa][cc], acc);
+        Y[r * D + j] = acc;
+      }
     __syncthreads();
   }
   __device__ static void phi_vec(const Sm& s, const double* x, double* y) {
@@ -152,8 +153,71 @@ struct Big {
     }
     __syncthreads();
   }
-  // EK1 / EK0 linearisation at eta[k+1] (statespace.cpp:65-103): thread 0
+  // EK1 / EK0 linearisation at eta[k+1] (statespace.cpp:65-103).  Pleiades
+  // (the only registered field with d = 28) is evaluated body-parallel (one
+  // thread per body owns its two acceleration rows of the Jacobian, the same
+  // summation order as field.cuh); other fields on thread 0.
   __device__ static void linearize(Sm& s, const BigArgs& a, int64_t k1) {
+    if (a.prob.kind == 5 && d == 28) {
+      constexpr int NB = 7;
+      for (int i = threadIdx.x; i < d * d; i += kBT) s.jac[i] = 0.0;
+      if (threadIdx.x < d) s.y[threadIdx.x] = a.eta[k1 * D + threadIdx.x * B];
+      if (threadIdx.x == 0) s.finite = 1;
+      __syncthreads();
+      const int t = threadIdx.x;
+      if (t < NB) {  // body i: f[2NB+i], f[3NB+i] and Jacobian rows 2NB+i, 3NB+i
+        const int i = t;
+        double ax = 0.0, ay = 0.0;
+        double* rx = s.jac + (2 * NB + i) * d;
+        double* ry = s.jac + (3 * NB + i) * d;
+        for (int j = 0; j < NB; ++j) {
+          if (j == i) continue;
+          const double dx = s.y[j] - s.y[i], dy = s.y[NB + j] - s.y[NB + i];
+          const double r2 = dx * dx + dy * dy;
+          const double r = sqrt(r2);
+          const double r3 = r2 * r, r5 = r3 * r2;
+          const double mj = static_cast<double>(j + 1);
+          ax += (mj * dx) / r3;
+          ay += (mj * dy) / r3;
+          const double dxx = mj * (1.0 / r3 - 3.0 * dx * dx / r5);
+          const double dxy = mj * (-3.0 * dx * dy / r5);
+          const double dyy = mj * (1.0 / r3 - 3.0 * dy * dy / r5);
+          rx[j] += dxx;
+          rx[i] -= dxx;
+          rx[NB + j] += dxy;
+          rx[NB + i] -= dxy;
+          ry[j] += dxy;
+          ry[i] -= dxy;
+          ry[NB + j] += dyy;
+          ry[NB + i] -= dyy;
+        }
+        s.f[2 * NB + i] = ax;
+        s.f[3 * NB + i] = ay;
+      } else if (t < 2 * NB) {  // positions' rows: x_i' = vx_i, y_i' = vy_i
+        const int i = t - NB;
+        s.f[i] = s.y[2 * NB + i];
+        s.f[NB + i] = s.y[3 * NB + i];
+        s.jac[i * d + 2 * NB + i] = 1.0;
+        s.jac[(NB + i) * d + 3 * NB + i] = 1.0;
+      }
+      __syncthreads();
+      if (t < d) {
+        bool fin = isfinite(s.f[t]);
+        double jy = 0.0;
+        for (int j = 0; j < d; ++j) {
+          if (!a.ek0) fin &= isfinite(s.jac[t * d + j]);
+          jy += s.jac[t * d + j] * s.y[j];
+        }
+        s.off[t] = a.ek0 ? s.f[t] : s.f[t] - jy;
+        if (!fin) s.finite = 0;
+      }
+      __syncthreads();
+      if (a.ek0) {
+        for (int i = threadIdx.x; i < d * d; i += kBT) s.jac[i] = 0.0;
+        __syncthreads();
+      }
+      return;
+    }
     if (threadIdx.x == 0) {
       for (int j = 0; j < d; ++j) s.y[j] = a.eta[k1 * D + j * B];
       double jac[d * d];
@@ -176,12 +240,12 @@ struct Big {
   // HX (d x D) = H_bar X; H_bar row i = t1 e_{iB+1} - t0 sum_c jac[i][c] e_{cB}
   __device__ static void h_rows(const Sm& s, const double* X, double* HX) {
     const double t0 = s.tn[0], t1 = s.tn[1];
-    for (int idx = threadIdx.x; idx < d * D; idx += kBT) {
-      const int i = idx / D, j = idx - (idx / D) * D;
-      double acc = (1.0 * t1) * X[(i * B + 1) * D + j];
-      for (int c = 0; c < d; ++c) acc = fma((-s.jac[i * d + c]) * t0, X[(c * B) * D + j], acc);
-      HX[idx] = acc;
-    }
+    for (int i = threadIdx.x >> 5; i < d; i += kBW)
+      for (int j = threadIdx.x & 31; j < D; j += 32) {
+        double acc = (1.0 * t1) * X[(i * B + 1) * D + j];
+        for (int c = 0; c < d; ++c) acc = fma((-s.jac[i * d + c]) * t0, X[(c * B) * D + j], acc);
+        HX[i * D + j] = acc;
+      }
     __syncthreads();
   }
   // XH (n x d) = X H_bar^T for X with n rows of D
@@ -206,6 +270,14 @@ struct Big {
     __syncthreads();
   }
 };
+
+// Dynamic shared memory of the kernels (big_la.cuh staging): two D x D
+// operands at stride D + 1 (trtri: L and its inverse; the chain's LU: the
+// matrix and D + 1 right-hand sides).
+template <int D>
+constexpr size_t big_smem_bytes(bool) {
+  return sizeof(double) * (size_t(D) * (D + 1) + size_t(D) * (D + 2));
+}
 
 // Per-chunk workspace slots (doubles), see the kernels.
 template <int D, int d>
@@ -343,7 +415,7 @@ __global__ void __launch_bounds__(kBT) k_big_chain_fwd(BigArgs a, const double* 
       X[i * (D + 1) + D] = acc;
     }
     __syncthreads();
-    lu_solve(D, M, D, D + 1, X, D + 1, red);  // X = [P_s | m_s]
+    lu_solve(D, M, D, D + 1, X, D + 1);  // X = [P_s | m_s]
     // out.m = A m_s + b; out.P = A P_s A^T + Pa
     for (int i = threadIdx.x; i < D; i += kBT) {
       double acc = bc[i];
@@ -707,10 +779,13 @@ __device__ void psd_factor(int n, double* A, int lda, double* F, int ldf, int* p
     }
     __syncthreads();
     // Schur complement on the remaining rows/cols
-    const int m = n - j - 1;
-    for (int idx = threadIdx.x; idx < m * m; idx += kBT) {
-      const int pi = perm[j + 1 + idx / m], pk = perm[j + 1 + idx % m];
-      A[pi * lda + pk] = fma(-F[pi * ldf + j], F[pk * ldf + j], A[pi * lda + pk]);
+    for (int ii = j + 1 + (threadIdx.x >> 5); ii < n; ii += kBW) {
+      const int pi = perm[ii];
+      const double fi = F[pi * ldf + j];
+      for (int kk = j + 1 + (threadIdx.x & 31); kk < n; kk += 32) {
+        const int pk = perm[kk];
+        A[pi * lda + pk] = fma(-fi, F[pk * ldf + j], A[pi * lda + pk]);
+      }
     }
     __syncthreads();
   }

@@ -19,9 +19,28 @@ struct BigEngine {
   using S = big::Slots<D, d>;
   static constexpr int B = D / d;
 
+  static void set_attrs() {
+    static OncePerDevice once;
+    once([] {
+      const int sm = int(big::big_smem_bytes<D>(false)), smc = int(big::big_smem_bytes<D>(true));
+      auto set = [](const void* f, int bytes) {
+        cuda_check(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "big smem");
+      };
+      set(reinterpret_cast<const void*>(big::k_big_fwd_reduce<D, d>), sm);
+      set(reinterpret_cast<const void*>(big::k_big_chain_fwd<D, d>), smc);
+      set(reinterpret_cast<const void*>(big::k_big_fwd_down<D, d, false>), sm);
+      set(reinterpret_cast<const void*>(big::k_big_fwd_down<D, d, true>), sm);
+      set(reinterpret_cast<const void*>(big::k_big_fin_fold<D, d>), sm);
+      set(reinterpret_cast<const void*>(big::k_big_chain_fin<D>), sm);
+      set(reinterpret_cast<const void*>(big::k_big_fin_bwd<D, d>), sm);
+    });
+  }
+
   static IeksResult run(pode_context* ctx, const host::Problem& p, const pode_prior& prior, const double* grid_h,
                         int64_t n1, const pode_ieks_config& cfg, double* means, double* cov, double* sol_m,
                         double* sol_c) {
+    set_attrs();
+    const size_t sm = big::big_smem_bytes<D>(false), smc = big::big_smem_bytes<D>(true);
     IeksSetup<D> s;
     IeksEngine<D>::setup(ctx, p, prior, grid_h, n1, s, false);
     cudaStream_t st = ctx->stream;
@@ -100,11 +119,11 @@ struct BigEngine {
       ++it;
       reset_error(ctx);
       a.eta = eta_a;
-      big::k_big_fwd_reduce<D, d><<<unsigned(nc), th, 0, st>>>(a, agg, 1);
+      big::k_big_fwd_reduce<D, d><<<unsigned(nc), th, sm, st>>>(a, agg, 1);
       note_launch(ctx, "big_fwd_reduce");
-      big::k_big_chain_fwd<D, d><<<1, th, 0, st>>>(a, agg, prefix, chain, 1, nullptr);
+      big::k_big_chain_fwd<D, d><<<1, th, smc, st>>>(a, agg, prefix, chain, 1, nullptr);
       note_launch(ctx, "big_chain_fwd");
-      big::k_big_fwd_down<D, d, false><<<unsigned(nc), th, 0, st>>>(a, prefix, E, g, g_term, bagg, nullptr, nullptr,
+      big::k_big_fwd_down<D, d, false><<<unsigned(nc), th, sm, st>>>(a, prefix, E, g, g_term, bagg, nullptr, nullptr,
                                                                     nullptr, 1, 1, nullptr);
       note_launch(ctx, "big_fwd_down");
       big::k_big_chain_bwd<D><<<1, th, 0, st>>>(nc, bagg, suffix, nullptr);
@@ -136,19 +155,19 @@ struct BigEngine {
     double* ps = ws.arr<double>("big_ps", size_t(nc) * DD);
     a.eta = eta_b;
     reset_error(ctx);
-    big::k_big_fwd_down<D, d, true><<<unsigned(nc), th, 0, st>>>(a, prefix, E, g, g_term, nullptr, pf, pterm, part, 1,
+    big::k_big_fwd_down<D, d, true><<<unsigned(nc), th, sm, st>>>(a, prefix, E, g, g_term, nullptr, pf, pterm, part, 1,
                                                                  1, nullptr);
     note_launch(ctx, "big_fin_fwd");
     k_finish3<<<1, kRedThreads, 0, st>>>(part, nc, red);
     note_launch(ctx, "finish3");
     IeksEngine<D>::check_linearization(ctx, s, it);
-    big::k_big_fin_fold<D, d><<<unsigned(nc), th, 0, st>>>(a, E, pf, pterm, sagg, 1);
+    big::k_big_fin_fold<D, d><<<unsigned(nc), th, sm, st>>>(a, E, pf, pterm, sagg, 1);
     note_launch(ctx, "big_fin_fold");
-    big::k_big_chain_fin<D><<<1, th, 0, st>>>(nc, sagg, ps, chain, nullptr);
+    big::k_big_chain_fin<D><<<1, th, sm, st>>>(nc, sagg, ps, chain, nullptr);
     note_launch(ctx, "big_chain_fin");
     const double count = double(N) * s.dim;
     big::BigOut o{means, cov, sol_m, sol_c};
-    big::k_big_fin_bwd<D, d><<<unsigned(nc), th, 0, st>>>(a, E, pf, pterm, ps, eta_a, red, count, o, 1);
+    big::k_big_fin_bwd<D, d><<<unsigned(nc), th, sm, st>>>(a, E, pf, pterm, ps, eta_a, red, count, o, 1);
     note_launch(ctx, "big_fin_bwd");
     cuda_check(cudaMemcpyAsync(ctx->h_scalars, red, sizeof(double), cudaMemcpyDeviceToHost, st), "innov");
     IeksEngine<D>::check_linearization(ctx, s, it);  // syncs
