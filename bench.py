@@ -209,6 +209,21 @@ def cpu_solve(problem_name, nu, n, threads):
     return r["seconds"], r["iterations"]
 
 
+def oracle_counts(problem, nu, log2n):
+    """The oracle's converged iteration counts for this exact configuration
+    from the committed fixtures (tests/golden, tools/make_fixtures.py):
+    seq_ieks and para_ieks(WorkPool 8) — at N = 2^20 the stopping rule is
+    rounding-determined, so counts differ between paths."""
+    tag = {"fhn": "fhn", "vanderpol": "vdp", "rigidbody": "rigid", "pleiades": "pleiades"}.get(problem, problem)
+    out = {}
+    for path, key in ((f"{tag}_q{nu}_n{log2n}_seq", "oracle_seq_ieks"), (f"{tag}_q{nu}_n{log2n}_par8", "oracle_para_ieks8")):
+        f = os.path.join(ROOT, "tests", "golden", path + ".npz")
+        if os.path.exists(f):
+            meta = json.loads(str(np.load(f)["meta"]))
+            out[key] = {"iterations": meta["iterations"], "converged": meta["converged"]}
+    return out
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -231,9 +246,12 @@ def run_reference(args):
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.problem} d={dim} IWP(q={args.nu}) D={dim * (args.nu + 1)}, "
                                    f"N=2^{args.log2n} uniform steps, IEKS to the reference stopping rule",
-                       "N": n, "iterations": iters,
-                       "note": f"bounded sample: full solves at N={n}; the N=2^{args.log2n} solve takes tens of "
-                               "minutes on CPU"},
+                       "N": n, "iterations": iters, "step_iterations_per_s": n * iters / t,
+                       "ms_per_iteration": t * 1e3 / max(iters, 1),
+                       "note": f"bounded sample: full solves at N={n} (a full N=2^{args.log2n} solve is "
+                               "~9 min seq_ieks / ~12.5 min para_ieks(8) on this class of host, "
+                               "tools/make_fixtures.py); compare per step-iteration with the GPU arm's "
+                               "config.step_iterations_per_s"},
             "cpu_baseline": {"value": v, "unit": "time-steps/s", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "time-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -411,6 +429,7 @@ def run_ours(args):
             "config": {"workload": f"{prob.name} d={d} IWP(q={nu}) D={D}, N=2^{args.log2n} uniform steps, "
                                    "IEKS to the reference stopping rule", "N": n, "iterations": iters,
                        "converged": converged, "step_iterations_per_s": value * iters / world,
+                       "ms_per_iteration": ms / max(iters, 1), **oracle_counts(args.problem, nu, args.log2n),
                        "parallelism": f"time-axis shards x{world} (gloo/nccl all-gather of chunk aggregates)"
                                       if shard else f"replicas x{world}",
                        "l2": "working set > L2 (126 MB) per solve"},

@@ -4,8 +4,11 @@
  * This is the drop-in boundary: a flat C interface (plain pointers and
  * sizes, no C++/torch types) whose entry points are what a binding of the
  * reference's C++ solver API (proj/include/paraode/) for this path needs.
- * The C++ mirror of that API (include/paraode/paraode.hpp) and the Python
- * package (paraode_b200/) both sit on top of it; see INTEGRATION.md.
+ * Three layers sit on top of it: the source-compatible
+ * C++ drop-in with the reference's own names and signatures
+ * (include/paraode/paraode.hpp), a templated C++ shim over any dense matrix
+ * type (include/paraode/paraode_b200.hpp), and the Python package
+ * (paraode_b200/).
  *
  * Conventions
  *   - All arithmetic is IEEE fp64.  All matrices are ROW-MAJOR and
@@ -61,7 +64,9 @@ typedef struct pode_context pode_context;
  * Not reentrant; distinct contexts may be used concurrently. */
 int pode_context_create(int32_t device, pode_context** out, pode_status* status);
 void pode_context_destroy(pode_context* ctx);
-/* Largest / smallest state dimension D compiled into this library. */
+/* Largest state dimension D compiled into this library: 112 for pode_ieks
+ * (the large-state engine serves d = 28, nu = 1..3: D = 56, 84, 112); the
+ * element operators, pode_rts, pode_eks and the sharded solve take D <= 16. */
 int32_t pode_max_state_dim(void);
 /* Number of kernels this library has launched on ctx (instrumentation). */
 int64_t pode_kernel_launches(const pode_context* ctx);

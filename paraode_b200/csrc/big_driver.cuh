@@ -119,6 +119,7 @@ struct BigEngine {
       ++it;
       reset_error(ctx);
       a.eta = eta_a;
+      NvtxRange nv("big_iteration");
       big::k_big_fwd_reduce<D, d><<<unsigned(nc), th, sm, st>>>(a, agg, 1);
       note_launch(ctx, "big_fwd_reduce");
       big::k_big_chain_fwd<D, d><<<1, th, smc, st>>>(a, agg, prefix, chain, 1, nullptr);

@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/paraode_b200.h"
 
 namespace pode {
@@ -123,6 +125,15 @@ inline void prof_record(pode_context* ctx, const char* name) {
   cuda_check(cudaEventRecord(e, ctx->stream), "profile record");
   ctx->prof.push_back({name, e});
 }
+
+// NVTX range over one IEKS stage (visible in Nsight Systems / ncu's NVTX
+// filters: --nvtx --nvtx-include "pass_C/"); header-only NVTX v3.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // PODE_TRACE_LAUNCHES=1 (debugging): synchronise after every launch and
 // name it on stderr, so a fault or hang is attributed to its kernel.

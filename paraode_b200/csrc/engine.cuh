@@ -564,7 +564,7 @@ constexpr bool bscan_fits() {
 // sequential fan-in (throughput-bound).  PODE_BSCAN=0 disables, =n sets it.
 inline int64_t bscan_max() {
   const char* env = std::getenv("PODE_BSCAN");
-  if (env == nullptr || *env == '\0') return 4096;
+  if (env == nullptr || *env == '\0') return 16384;  // tools/knob_sweep.py (ms per iteration)
   const long long v = std::atoll(env);
   return v == 1 ? (int64_t(1) << 62) : int64_t(v);
 }

@@ -276,7 +276,7 @@ struct FastEngine {
   // ⊗_f needs ~250 live doubles per thread and spills.
   static int scan_fanin() {
     const char* env = std::getenv("PODE_SCAN_FANIN");
-    const int v = (env && *env) ? std::atoi(env) : 4;
+    const int v = (env && *env) ? std::atoi(env) : 8;  // tools/knob_sweep.py: 8 is fastest per iteration
     return v >= 2 ? v : 4;
   }
 
@@ -369,14 +369,30 @@ struct FastEngine {
         ag.eta = eta_a;
         ag.eta_term = term(eta_a);
       }
-      Pass::fwd_reduce(st, ag, cst, agg);
-      note_launch(ctx, "fast_fwd_reduce");
-      const ScanTally tf = Engine<D>::scan_filtering_gauss(ctx, nc, agg, agg, scan_fanin());
-      Pass::fwd_down(st, ag, cst, agg, soa, bagg);
-      note_launch(ctx, "fast_fwd_down");
-      const ScanTally tr = Engine<D>::scan_means_terminal(ctx, nc, bagg, scan_fanin());
-      Pass::template bwd_down<false>(st, ag, cst, soa, bagg, eta_a, term(eta_a), eta_b, term(eta_b), part);
-      note_launch(ctx, "fast_bwd_down");
+      {
+        NvtxRange r("pass_A_chunk_fold");
+        Pass::fwd_reduce(st, ag, cst, agg);
+        note_launch(ctx, "fast_fwd_reduce");
+      }
+      ScanTally tf, tr;
+      {
+        NvtxRange r("pass_B_aggregate_scan");
+        tf = Engine<D>::scan_filtering_gauss(ctx, nc, agg, agg, scan_fanin());
+      }
+      {
+        NvtxRange r("pass_C_filter_smoothing_elements");
+        Pass::fwd_down(st, ag, cst, agg, soa, bagg);
+        note_launch(ctx, "fast_fwd_down");
+      }
+      {
+        NvtxRange r("pass_D_backward_scan");
+        tr = Engine<D>::scan_means_terminal(ctx, nc, bagg, scan_fanin());
+      }
+      {
+        NvtxRange r("pass_E_backward_means_objective");
+        Pass::template bwd_down<false>(st, ag, cst, soa, bagg, eta_a, term(eta_a), eta_b, term(eta_b), part);
+        note_launch(ctx, "fast_bwd_down");
+      }
       if (graph) {
         k_finish_iter<<<1, kRedThreads, 0, st>>>(part, nparts, ls, trace_dev, ctx->d_err, h);
         note_launch(ctx, "finish_iter");
@@ -709,6 +725,7 @@ struct FastEngine {
     const size_t padded = size_t(nc) * a.L;
     double* cf = ws.arr<double>("fin_cf", padded * D * D + D * D);
     double* cterm = cf + padded * D * D;
+    NvtxRange nv("finalize_covariances_outputs");
     const unsigned lblocks = Pass::blocks(nc);
     double* part = ws.arr<double>("fin_part", size_t(lblocks) * 3 + 3);
     double* red = part + size_t(lblocks) * 3;

@@ -31,6 +31,12 @@ constexpr int kLaneThreads = 128;
 #define PODE_BWD_MIN_BLOCKS 2
 #endif
 constexpr int kBwdMinBlocks = PODE_BWD_MIN_BLOCKS;
+// Passes A and C: resident 128-thread blocks per SM the register allocation
+// targets (1 = up to 255 registers).
+#ifndef PODE_LANE_MIN_BLOCKS
+#define PODE_LANE_MIN_BLOCKS 1
+#endif
+constexpr int kLaneMinBlocks = PODE_LANE_MIN_BLOCKS;
 
 // Householder LQ of an R x K row-major register matrix over the first P
 // pivots: row p is reflected against columns p..K-1 and every later row is
@@ -423,7 +429,7 @@ __device__ __forceinline__ void block_sum_partial(double* red, double v, double*
 // One thread per chunk: fold the chunk's filtering elements into the
 // aggregate (A, b, C, eta, J) (see fast.cuh for the algebra).
 template <int D, int d>
-__global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_reduce(const FastArgs a, FastConst<D> cst, FEd agg) {
+__global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks) k_lane_fwd_reduce(const FastArgs a, FastConst<D> cst, FEd agg) {
   using M = Model<D, d>;
   constexpr int B = M::B;
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -744,7 +750,7 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
 }
 
 template <int D, int d, bool kFinal = false>
-__global__ void __launch_bounds__(kLaneThreads) k_lane_fwd_down(const FastArgs a, FastConst<D> cst, FEd prefix,
+__global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks) k_lane_fwd_down(const FastArgs a, FastConst<D> cst, FEd prefix,
                                                                 ElemSoA elems, double* cf = nullptr,
                                                                 double* cterm = nullptr, double* part = nullptr,
                                                                 SEd bagg = SEd{}) {

@@ -78,7 +78,7 @@ def test_null_context_is_rejected():
     st = abi.Status()
     rc = lib.pode_rts(None, None, abi.RtsOut(), None, C.byref(st))
     assert rc == 1 and b"NULL context" in st.msg
-    assert lib.pode_max_state_dim() == 16
+    assert lib.pode_max_state_dim() == 112  # pode_ieks: the large-state engine (Pleiades, D = 112)
 
 
 def test_problem_registry_and_grid_helpers():

@@ -56,7 +56,12 @@ def test_pleiades_2e10_fixture():
     compare(got, z, meta, "pleiades q3 N=2^10 (fixture)", alternatives(P, meta, meta["iterations"]))
 
 
-def test_pleiades_converged_fixture():
+def test_pleiades_default_rule_outcome_matches_oracle():
+    """The reference stopping rule on Pleiades from the constant initial
+    trajectory (ieks.cpp:145-148) at N = 2^10: the oracle's seq_ieks does not
+    converge within the 100-iteration budget — the Gauss-Newton iterates
+    diverge (objective ~1e19) — and neither does the GPU; the traces agree
+    while the iterates are still determined (first 3 iterations)."""
     path = os.path.join(GOLDEN, "pleiades_q3_n10_seq.npz")
     if not os.path.exists(path):
         pytest.skip("fixture not generated")
@@ -64,9 +69,10 @@ def test_pleiades_converged_fixture():
     meta = json.loads(str(z["meta"]))
     conv = gpu_solve(P, meta)
     print(f"pleiades q3 N=2^10 default rule: GPU {conv.iterations} its conv={conv.converged}; "
-          f"oracle {meta['iterations']} its conv={meta['converged']}")
-    got = gpu_solve(P, meta, max_iterations=meta["iterations"], **NEVER)
-    compare(got, z, meta, "pleiades q3 N=2^10 converged (fixture)", alternatives(P, meta, meta["iterations"]))
+          f"oracle {meta['iterations']} its conv={meta['converged']}; final objective GPU "
+          f"{conv.objective_trace[-1]:.3e}, oracle {z['objective_trace'][-1]:.3e}")
+    assert conv.converged == meta["converged"] and conv.iterations == meta["iterations"]
+    assert np.allclose(conv.objective_trace[:3], z["objective_trace"][:3], rtol=1e-8)
 
 
 def test_pleiades_errors_and_determinism():
