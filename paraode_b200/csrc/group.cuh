@@ -298,25 +298,28 @@ struct Reflector {
 // approximation refined by Newton steps to full double precision (no
 // IEEE slow-path calls, so a whole Householder sweep stays one basic block).
 // Inputs are positive normal numbers here (guarded by the callers).
+// PODE_NEWTON_ITERS refinements (the MUFU seed has ~2^-23 relative error,
+// Newton squares it: two steps reach 2^-46 -> 2^-92, below fp64 rounding).
+#ifndef PODE_NEWTON_ITERS
+#define PODE_NEWTON_ITERS 2
+#endif
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
-  y = y * fma(-hx * y, y, 1.5);
-  y = y * fma(-hx * y, y, 1.5);
+#pragma unroll
+  for (int i = 0; i < PODE_NEWTON_ITERS; ++i) y = y * fma(-hx * y, y, 1.5);
   return y;
 }
 
 __device__ __forceinline__ double rcp_nr(double x) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
+#pragma unroll
+  for (int i = 0; i < PODE_NEWTON_ITERS; ++i) {
+    const double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+  }
   return y;
 }
 
