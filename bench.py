@@ -291,6 +291,10 @@ def run_ours(args):
     grid_pinned = torch.from_numpy(grid).pin_memory()
     cfg = P.IeksConfig()
     gather = P.torch_allgather() if shard else None
+    device_exchange = shard and os.environ.get("PODE_BENCH_BACKEND", "nccl") == "nccl"
+    if device_exchange:  # ncclAllGather inside the library on device buffers: no host staging per exchange
+        P.torch_nccl_bind(ctx)
+        gather = None
 
     def solve_device():
         ptr = [C.cast(C.c_void_p(t.data_ptr()), A.dptr) for t in out_dev]
@@ -303,7 +307,8 @@ def run_ours(args):
         st = A.Status()
         gp = C.cast(C.c_void_p(grid_pinned.data_ptr()), A.dptr)
         if shard:
-            comm, failure = P.api.make_shard_comm(rank, world, gather)
+            comm, failure = ((A.ShardComm(rank, world, A.ALLGATHER_FN(), None), []) if gather is None
+                             else P.api.make_shard_comm(rank, world, gather))
             rc = ctx._lib.pode_ieks_sharded(ctx.handle, C.byref(pr), C.byref(prior), gp, n1, C.byref(c),
                                             C.byref(comm), C.byref(rep), C.byref(st))
             if failure:
@@ -430,7 +435,9 @@ def run_ours(args):
                                    "IEKS to the reference stopping rule", "N": n, "iterations": iters,
                        "converged": converged, "step_iterations_per_s": value * iters / world,
                        "ms_per_iteration": ms / max(iters, 1), **oracle_counts(args.problem, nu, args.log2n),
-                       "parallelism": f"time-axis shards x{world} (gloo/nccl all-gather of chunk aggregates)"
+                       "parallelism": (f"time-axis shards x{world} (" +
+                                       ("in-library ncclAllGather of chunk aggregates on device buffers"
+                                        if device_exchange else "host all-gather callback") + ")")
                                       if shard else f"replicas x{world}",
                        "l2": "working set > L2 (126 MB) per solve"},
             "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof,

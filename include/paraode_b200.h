@@ -280,6 +280,19 @@ typedef struct {
   void* user;
 } pode_shard_comm;
 
+/* Device-side exchange (no host staging): bind an NCCL communicator to the
+ * context; pode_ieks_sharded then all-gathers the chunk aggregates and
+ * stopping scalars with ncclAllGather on device buffers on the context
+ * stream, and comm->allgather may be NULL.  NCCL is loaded at run time
+ * (dlopen of `nccl_path`, e.g. the libnccl.so.2 torch bundles; NULL: the
+ * loader's search path).  pode_nccl_unique_id makes the 128-byte
+ * ncclUniqueId on one rank; the caller broadcasts it to every rank (any
+ * transport) before each rank calls pode_context_nccl_init.  One process
+ * per GPU (NCCL rejects two ranks on one device). */
+int pode_nccl_unique_id(const char* nccl_path, uint8_t id[128], pode_status* status);
+int pode_context_nccl_init(pode_context* ctx, const char* nccl_path, const uint8_t id[128], int32_t rank,
+                           int32_t ranks, pode_status* status);
+
 /* Shard node range of `rank` (first node, number of reported nodes). */
 void pode_shard_range(int64_t n_nodes, int32_t rank, int32_t ranks, int64_t* first_node, int64_t* count);
 

@@ -76,6 +76,9 @@ SYMBOLS = {
     "pode_kernel_launches": (C.c_int64, [C.c_void_p]),
     "pode_context_stream": (C.c_void_p, [C.c_void_p]),
     "pode_context_set_option": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
+    "pode_nccl_unique_id": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint8), C.POINTER(Status)]),
+    "pode_context_nccl_init": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_uint8), C.c_int32, C.c_int32,
+                                         C.POINTER(Status)]),
     "pode_profile": (C.c_int, [C.c_void_p, C.c_int32]),
     "pode_profile_read": (C.c_int64, [C.c_void_p, C.c_char_p, C.c_int64]),
     "pode_make_filtering_elements": (C.c_int, [C.c_void_p, C.POINTER(Chain), C.c_int32,

@@ -101,6 +101,14 @@ class Context:
         if rc != 0:
             raise InvalidInputError(f"pode_context_set_option({option}, {value}) rejected")
 
+    def nccl_init(self, unique_id: bytes, rank: int, ranks: int, nccl_path: Optional[str] = None):
+        """Bind an NCCL communicator (pode_context_nccl_init): the sharded
+        solve then exchanges on the device (ncclAllGather), no host staging."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(unique_id))
+        st = A.Status()
+        _raise(self._lib.pode_context_nccl_init(self._h, _nccl_path(nccl_path), buf, int(rank), int(ranks),
+                                                C.byref(st)), st)
+
     def set_chunk_len(self, steps: int):
         self.set_option(self.OPT_CHUNK_LEN, steps)
 
@@ -610,6 +618,39 @@ def torch_allgather(group=None):
     return gather
 
 
+def _nccl_path(path=None):
+    """libnccl.so.2: explicit, else the one torch bundles (nvidia/nccl/lib)."""
+    if path:
+        return path.encode()
+    import os
+    try:
+        import torch
+        cand = os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "nccl", "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            return os.path.abspath(cand).encode()
+    except Exception:
+        pass
+    return None
+
+
+def nccl_unique_id(nccl_path: Optional[str] = None) -> bytes:
+    """A fresh 128-byte ncclUniqueId (pode_nccl_unique_id)."""
+    buf = (C.c_uint8 * 128)()
+    st = A.Status()
+    _raise(A.load().pode_nccl_unique_id(_nccl_path(nccl_path), buf, C.byref(st)), st)
+    return bytes(buf)
+
+
+def torch_nccl_bind(ctx, group=None, nccl_path: Optional[str] = None):
+    """Device-side shard exchange for para_ieks_sharded: rank 0 makes the
+    NCCL id, torch.distributed broadcasts it, every rank binds its context."""
+    import torch.distributed as dist
+    rank, ranks = dist.get_rank(group), dist.get_world_size(group)
+    obj = [nccl_unique_id(nccl_path) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    ctx.nccl_init(obj[0], rank, ranks, nccl_path)
+
+
 def make_shard_comm(rank: int, ranks: int, allgather):
     """pode_shard_comm for a Python all-gather (send ndarray -> rank-ordered
     ndarray).  Returns (comm, failures); keep comm alive during the call."""
@@ -652,7 +693,9 @@ def para_ieks_sharded(ivp: InitialValueProblem, prior: IwpPrior, grid: Sequence[
                       allgather, config: IeksConfig = IeksConfig(), want_cov=True, ctx=None) -> ShardReport:
     """para_ieks over the time-axis shard `rank` of `ranks` (one process per
     GPU).  `allgather(send: ndarray) -> ndarray` gathers every
-    rank's equally sized float64 vector in rank order (torch_allgather())."""
+    rank's equally sized float64 vector in rank order (torch_allgather());
+    None when the context has an NCCL communicator (torch_nccl_bind): the
+    exchanges then stay on the device."""
     c = _ctx(ctx)
     grid = _f64(grid)
     n1 = grid.shape[0]
@@ -665,7 +708,10 @@ def para_ieks_sharded(ivp: InitialValueProblem, prior: IwpPrior, grid: Sequence[
     trace = np.zeros(max(config.max_iterations, 1))
     rep = A.IeksReport(_p(means), _p(cov), _p(sm), _p(sc), _p(trace), trace.shape[0], A.PODE_HOST,
                        0, 0, 0.0, A.ScanStats())
-    comm, failure = make_shard_comm(rank, ranks, allgather)
+    if allgather is None:
+        comm, failure = A.ShardComm(rank, ranks, A.ALLGATHER_FN(), None), []
+    else:
+        comm, failure = make_shard_comm(rank, ranks, allgather)
     pr = ivp._c()
     prior_c = A.Prior(prior.nu, prior.dim, prior.sigma)
     lin = {"ek1": 0, "ek0": 1}[config.linearization]

@@ -15,6 +15,7 @@
 #include "host_model.hpp"
 #include "field.cuh"
 #include "ieks.cuh"
+#include "nccl.hpp"
 
 namespace pode {
 
@@ -351,6 +352,7 @@ void pode_context_destroy(pode_context* ctx) {
   if (ctx == nullptr) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  nccl::destroy(ctx);
   for (auto& kv : ctx->graphs) {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
@@ -415,6 +417,33 @@ int64_t pode_profile_read(pode_context* ctx, char* buf, int64_t size) {
 int64_t pode_kernel_launches(const pode_context* ctx) { return ctx ? ctx->launches : 0; }
 
 void* pode_context_stream(pode_context* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int pode_nccl_unique_id(const char* nccl_path, uint8_t id[128], pode_status* status) {
+  return guarded(status, [&] {
+    if (id == nullptr) throw ApiError(PODE_ERR_INVALID_INPUT, "NULL id");
+    nccl::UniqueId u;
+    nccl::check(nccl::api(nccl_path).get_unique_id(&u), "ncclGetUniqueId");
+    std::memcpy(id, u.internal, sizeof(u.internal));
+  });
+}
+
+int pode_context_nccl_init(pode_context* ctx, const char* nccl_path, const uint8_t id[128], int32_t rank,
+                           int32_t ranks, pode_status* status) {
+  return guarded(status, [&] {
+    check_ctx(ctx);
+    if (id == nullptr || ranks < 1 || rank < 0 || rank >= ranks)
+      throw ApiError(PODE_ERR_INVALID_INPUT, "nccl_init: need an id and 0 <= rank < ranks");
+    nccl::Api& a = nccl::api(nccl_path);
+    nccl::destroy(ctx);
+    nccl::UniqueId u;
+    std::memcpy(u.internal, id, sizeof(u.internal));
+    nccl::Comm comm = nullptr;
+    nccl::check(a.comm_init_rank(&comm, ranks, u, rank), "ncclCommInitRank");
+    ctx->nccl_comm = comm;
+    ctx->nccl_rank = rank;
+    ctx->nccl_ranks = ranks;
+  });
+}
 
 int pode_context_set_option(pode_context* ctx, int32_t option, int64_t value) {
   if (ctx == nullptr) return PODE_ERR_INVALID_INPUT;
@@ -688,8 +717,10 @@ int pode_ieks_sharded(pode_context* ctx, const pode_problem* problem, const pode
   return guarded(status, [&] {
     check_ctx(ctx);
     if (problem == nullptr || prior == nullptr || grid == nullptr || config == nullptr || report == nullptr ||
-        comm == nullptr || comm->allgather == nullptr)
+        comm == nullptr || (comm->allgather == nullptr && ctx->nccl_comm == nullptr))
       throw ApiError(PODE_ERR_INVALID_INPUT, "ieks_sharded: NULL argument");
+    if (ctx->nccl_comm && (ctx->nccl_rank != comm->rank || ctx->nccl_ranks != comm->ranks))
+      throw ApiError(PODE_ERR_INVALID_INPUT, "ieks_sharded: rank / ranks disagree with the context's NCCL communicator");
     if (comm->ranks < 1 || comm->rank < 0 || comm->rank >= comm->ranks)
       throw ApiError(PODE_ERR_INVALID_INPUT, "ieks_sharded: rank outside [0, ranks)");
     const host::Problem p = host::resolve_problem(*problem);

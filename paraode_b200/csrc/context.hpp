@@ -87,6 +87,9 @@ struct pode_context {
   unsigned long long* h_err = nullptr;  // pinned mirror
   double* h_scalars = nullptr;          // pinned scalars (reductions)
   int64_t launches = 0;
+  // pode_context_nccl_init: device-side shard exchange (nccl.hpp)
+  void* nccl_comm = nullptr;
+  int nccl_rank = 0, nccl_ranks = 0;
   // pode_context_set_option (0 = automatic / environment default)
   int64_t opt_chunk = 0;
   int opt_engine = 0;

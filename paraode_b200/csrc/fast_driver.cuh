@@ -13,6 +13,7 @@
 #include "grp_fused.cuh"
 #include "ieks.cuh"
 #include "lane.cuh"
+#include "nccl.hpp"
 
 namespace pode {
 
@@ -68,6 +69,20 @@ static __global__ void k_finish_iter(const double* part, int64_t nparts, LoopSta
   const bool failed = *err != ~0ull;
   cudaGraphSetConditional(h, (!conv && !failed && ls->it < ls->max_it) ? 1u : 0u);
 }
+
+// Packed device moves of up to five fields (one launch per element move of
+// the shard exchanges) and a one-double store.
+struct MoveSpec {
+  const double* src[5];
+  double* dst[5];
+  int len[5];
+  int nfields;
+};
+static __global__ void k_move_fields(MoveSpec m) {
+  for (int f = 0; f < m.nfields; ++f)
+    for (int i = threadIdx.x; i < m.len[f]; i += blockDim.x) m.dst[f][i] = m.src[f][i];
+}
+static __global__ void k_set_scalar(double* p, double v) { *p = v; }
 
 // Launch policies of the fused iteration: the lane-serial passes (lane.cuh,
 // one chunk per thread, chunk-interleaved HBM layout; D <= 9) and the
@@ -471,28 +486,46 @@ struct FastEngine {
     if (src == nullptr || dst == nullptr) return;
     cuda_check(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream), "shard copy");
   }
+  // Element i of src -> element j of dst, every field in one launch.
   static void fel_move(pode_context* ctx, const FEd& src, int64_t i, const FEd& dst, int64_t j) {
-    d2d(ctx, dst.a + j * D * D, src.a + i * D * D, D * D);
-    d2d(ctx, dst.c + j * D * D, src.c + i * D * D, D * D);
-    d2d(ctx, dst.j + j * D * D, src.j + i * D * D, D * D);
-    d2d(ctx, dst.b + j * D, src.b + i * D, D);
-    d2d(ctx, dst.eta + j * D, src.eta + i * D, D);
+    k_move_fields<<<1, 128, 0, ctx->stream>>>(
+        MoveSpec{{src.a + i * D * D, src.c + i * D * D, src.j + i * D * D, src.b + i * D, src.eta + i * D},
+                 {dst.a + j * D * D, dst.c + j * D * D, dst.j + j * D * D, dst.b + j * D, dst.eta + j * D},
+                 {D * D, D * D, D * D, D, D}, 5});
+    note_launch(ctx, "move");
   }
   static void sel_move(pode_context* ctx, const SEd& src, int64_t i, const SEd& dst, int64_t j, bool with_l) {
-    d2d(ctx, dst.e + j * D * D, src.e + i * D * D, D * D);
-    d2d(ctx, dst.g + j * D, src.g + i * D, D);
-    if (with_l) d2d(ctx, dst.l + j * D * D, src.l + i * D * D, D * D);
+    k_move_fields<<<1, 128, 0, ctx->stream>>>(
+        MoveSpec{{src.e + i * D * D, src.g + i * D, with_l ? src.l + i * D * D : nullptr, nullptr, nullptr},
+                 {dst.e + j * D * D, dst.g + j * D, with_l ? dst.l + j * D * D : nullptr, nullptr, nullptr},
+                 {D * D, D, with_l ? D * D : 0, 0, 0}, with_l ? 3 : 2});
+    note_launch(ctx, "move");
   }
 
   // All-gather of one contiguous device element (count doubles) from every
-  // shard; the R copies land contiguously in dev_all (rank order).
+  // shard; the R copies land contiguously in dev_all (rank order).  With an
+  // NCCL communicator on the context (pode_context_nccl_init) the exchange
+  // stays on the device (ncclAllGather on the context stream); otherwise it
+  // goes through the caller's host all-gather callback.
   static void gather(pode_context* ctx, const pode_shard_comm& comm, const double* dev_own, int64_t count,
                      double* dev_all, std::vector<double>* host_all = nullptr) {
+    if (ctx->nccl_comm) {
+      double* recv = dev_all ? dev_all : ctx->ws.arr<double>("sh_recv", size_t(count) * comm.ranks);
+      nccl::all_gather(ctx, dev_own, count, recv);
+      if (host_all) {  // the stopping scalars: the decision is taken on the host
+        host_all->resize(size_t(count) * comm.ranks);
+        cuda_check(cudaMemcpyAsync(host_all->data(), recv, sizeof(double) * host_all->size(), cudaMemcpyDeviceToHost,
+                                   ctx->stream),
+                   "shard scalars");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "shard sync");
+      }
+      return;
+    }
     std::vector<double> send(static_cast<size_t>(count)), recv(static_cast<size_t>(count) * comm.ranks);
     cuda_check(cudaMemcpyAsync(send.data(), dev_own, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream),
                "shard send");
     cuda_check(cudaStreamSynchronize(ctx->stream), "shard sync");
-    if (comm.allgather(comm.user, send.data(), count, recv.data()) != 0)
+    if (comm.allgather == nullptr || comm.allgather(comm.user, send.data(), count, recv.data()) != 0)
       throw ApiError(PODE_ERR_INVALID_INPUT, "ieks_sharded: all-gather failed");
     if (dev_all)
       cuda_check(cudaMemcpyAsync(dev_all, recv.data(), sizeof(double) * recv.size(), cudaMemcpyHostToDevice,
@@ -507,8 +540,8 @@ struct FastEngine {
                       bool& any_failed, bool own_failed) {
     double* tmp = ctx->ws.arr<double>("sh_s3", 4);
     cuda_check(cudaMemcpyAsync(tmp, dev3, sizeof(double) * 3, cudaMemcpyDeviceToDevice, ctx->stream), "s3");
-    const double flag = own_failed ? 1.0 : 0.0;
-    cuda_check(cudaMemcpyAsync(tmp + 3, &flag, sizeof(double), cudaMemcpyHostToDevice, ctx->stream), "s3 flag");
+    k_set_scalar<<<1, 1, 0, ctx->stream>>>(tmp + 3, own_failed ? 1.0 : 0.0);
+    note_launch(ctx, "flag");
     std::vector<double> all;
     gather(ctx, comm, tmp, 4, nullptr, &all);
     out[0] = 0.0;

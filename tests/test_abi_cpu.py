@@ -91,3 +91,14 @@ def test_problem_registry_and_grid_helpers():
         P.problem_by_name("lorenz")
     assert P.problem_by_name("fhn").dim == 2 and P.pleiades().dim == 28
     assert np.array_equal(P.affine(np.eye(2), [1, 2], [0, 0], 1.0).params, [1, 0, 0, 1, 1, 2])
+
+
+def test_nccl_unique_id_without_gpu():
+    """The device-exchange setup (pode_nccl_unique_id) loads NCCL at run time
+    (torch's bundled libnccl.so.2) and makes a 128-byte id on the host."""
+    import paraode_b200 as P
+    try:
+        uid = P.nccl_unique_id()
+    except P.UnsupportedError:
+        pytest.skip("NCCL not loadable here")
+    assert isinstance(uid, bytes) and len(uid) == 128 and any(uid)

@@ -104,3 +104,22 @@ def test_single_shard_equals_para_ieks():
     assert b.iterations == a.iterations and b.first_node == 0
     assert rel(b.means, a.means) <= 1e-12
     assert rel(dense_cov(b.cov_sqrt), dense_cov(a.cov_sqrt)) <= 1e-10
+
+
+def test_single_shard_device_exchange_over_nccl():
+    """The device-side exchange (pode_context_nccl_init: ncclAllGather on the
+    context stream, no host staging, comm->allgather NULL) on a one-rank NCCL
+    communicator — NCCL rejects two ranks on one GPU, so the multi-rank
+    device path runs on multi-GPU nodes only; its exchange sequence is the
+    one the gloo tests above verify."""
+    prob = P.fitzhugh_nagumo()
+    grid = P.uniform_grid(prob.t_end, 3000)
+    ctx = P.Context()
+    ctx.nccl_init(P.nccl_unique_id(), 0, 1)
+    got = P.para_ieks_sharded(prob, P.IwpPrior(2, 2, 1.0), grid, 0, 1, None, ctx=ctx)
+    want = O.ieks(O.problem("fhn"), 2, O.uniform_grid(prob.t_end, 3000), mode=0)
+    assert got.iterations == want["iterations"] and got.converged
+    assert rel(got.means, want["means"]) <= 1e-9
+    assert rel(dense_cov(got.cov_sqrt), dense_cov(want["cov_sqrt"])) <= 1e-7
+    with pytest.raises(P.InvalidInputError):  # rank / ranks must match the communicator
+        P.para_ieks_sharded(prob, P.IwpPrior(2, 2, 1.0), grid, 0, 2, None, ctx=ctx)
