@@ -122,6 +122,22 @@ struct Big {
     }
     __syncthreads();
   }
+  // Y = Phi X + M on and below the diagonal, mirrored above: the predicted
+  // covariance phi (P phi^T) + Q Q^T, exactly symmetric (the two triangles
+  // of phi P phi^T would otherwise differ by the association order).
+  __device__ static void phi_rows_sym(const Sm& s, const double* X, const double* M, double* Y) {
+    for (int r = threadIdx.x >> 5; r < D; r += kBW) {
+      const int blk = r / B, a = r - blk * B;
+      for (int j = threadIdx.x & 31; j <= r; j += 32) {
+        double acc = 0.0;
+        for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[(blk * B + i) * D + j], acc);
+        acc += M[r * D + j];
+        Y[r * D + j] = acc;
+        Y[j * D + r] = acc;
+      }
+    }
+    __syncthreads();
+  }
   // Y = X Phi^T (columns), Y != X
   __device__ static void phi_cols(const Sm& s, const double* X, double* Y) {
     for (int r = threadIdx.x >> 5; r < D; r += kBW)
@@ -337,9 +353,7 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_reduce(BigArgs a, double* agg, 
     G::phi_rows(s, Am, Anew);  // A- = phi A
     G::phi_vec(s, bv, bm);     // b- = phi b
     G::phi_cols(s, P, T1);     // P phi^T
-    G::phi_rows(s, T1, Pm);    // phi P phi^T
-    for (int idx = threadIdx.x; idx < D * D; idx += kBT) Pm[idx] += a.qq[idx];
-    __syncthreads();
+    G::phi_rows_sym(s, T1, a.qq, Pm);  // phi P phi^T + Q Q^T
     G::linearize(s, a, k + 1);
     if (!s.finite && bad_lin < 0) bad_lin = k + 1;
     bad_sing |= cov_update_parts<D, d>(s, Pm, HP, Sd, Sinv, W);
@@ -351,8 +365,7 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_reduce(BigArgs a, double* agg, 
     // eta -= Ubar^T ubar; Lambda += Ubar^T Ubar
     gemm<true, false>(D, D, d, -1.0, W, D, Ub, D, 1.0, Anew, D);
     gemv<true>(D, d, -1.0, W, D, ub, 1.0, bm);
-    gemm<true, false>(D, D, d, -1.0, W, D, W, D, 1.0, Pm, D);
-    symmetrize(D, Pm, D);
+    gemm<true, false>(D, D, d, -1.0, W, D, W, D, 1.0, Pm, D);  // (P stays symmetric to rounding; the chains re-symmetrise)
     gemv<true>(D, d, -1.0, Ub, D, ub, 1.0, eta);
     gemm<true, false>(D, D, d, 1.0, Ub, D, Ub, D, 1.0, Lam, D);
     double* t = Am;  // rotate buffers: A <- Anew, P <- Pm
@@ -459,22 +472,17 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_down(BigArgs a, const double* p
     G::step_consts(s, a.grid, k);
     if constexpr (kFinal) copy(D * D, P, pf + k * S::DD);
     G::phi_cols(s, P, Y);   // Y = P phi^T
-    G::phi_rows(s, Y, Pm);  // Pm = phi P phi^T + Q Q^T
-    for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
-      Pm[idx] += a.qq[idx];
-      Lc[idx] = Pm[idx];
-    }
-    __syncthreads();
+    G::phi_rows_sym(s, Y, a.qq, Pm);  // Pm = phi P phi^T + Q Q^T
+    copy(D * D, Pm, Lc);
     bad_sing |= potrf(D, Lc, D, s.red);                                // Pm = L L^T
     trtri_lower(D, Lc, D, Li, D);                                      // L^-1
     gemm<false, true>(D, D, D, 1.0, Y, D, Li, D, 0.0, Z, D);           // Y L^-T
     double* Ek = E_out + k * S::DD;
     gemm<false, false>(D, D, D, 1.0, Z, D, Li, D, 0.0, Ek, D);         // E = Y L^-T L^-1
     G::phi_vec(s, m, mm);                                              // m- = phi m
+    gemv<false>(D, D, -1.0, Ek, D, mm, 0.0, gk);                       // -E m-
     for (int r = threadIdx.x; r < D; r += kBT) {
-      double acc = 0.0;
-      for (int j = 0; j < D; ++j) acc = fma(Ek[r * D + j], mm[j], acc);
-      gk[r] = m[r] - acc;
+      gk[r] += m[r];                                                   // g = m - E phi m
       g_out[k * D + r] = gk[r];
     }
     __syncthreads();
@@ -504,7 +512,6 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_down(BigArgs a, const double* p
     copy(D, mm, m);
     gemv<true>(D, d, -1.0, W, D, zb, 1.0, m);       // m+ = m- - W^T S^-1 z
     gemm<true, false>(D, D, d, -1.0, W, D, W, D, 1.0, Pm, D);  // P+ = Pm - W^T W
-    symmetrize(D, Pm, D);
     double* t = P;
     P = Pm;
     Pm = t;

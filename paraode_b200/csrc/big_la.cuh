@@ -118,8 +118,16 @@ __device__ void gemv(int M, int K, double alpha, const double* A, int lda, const
   } else {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = warp; i < M; i += kBW) {
-      double acc = 0.0;
-      for (int k = lane; k < K; k += 32) acc = fma(A[i * lda + k], x[k], acc);
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // independent chains: loads in flight
+      int k = lane;
+      for (; k + 96 < K; k += 128) {
+        a0 = fma(A[i * lda + k], x[k], a0);
+        a1 = fma(A[i * lda + k + 32], x[k + 32], a1);
+        a2 = fma(A[i * lda + k + 64], x[k + 64], a2);
+        a3 = fma(A[i * lda + k + 96], x[k + 96], a3);
+      }
+      for (; k < K; k += 32) a0 = fma(A[i * lda + k], x[k], a0);
+      double acc = (a0 + a1) + (a2 + a3);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) y[i] = (beta == 0.0) ? alpha * acc : fma(alpha, acc, beta * y[i]);
