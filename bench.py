@@ -63,8 +63,8 @@ def peaks():
         pass
     fp64, fp64_src = FP64_FALLBACK_TFS, "fallback (nominal)"
     try:
-        fp64 = float(json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")))["fp64_fma_tflops"])
-        fp64_src = "measured DFMA (profiles/r01_fp64_peak.json)"
+        fp64 = float(json.load(open(os.path.join(ROOT, "profiles", "r02_fp64_peak.json")))["fp64_fma_tflops"])
+        fp64_src = "measured DFMA (profiles/r02_fp64_peak.json, clocks recorded)"
     except Exception:
         pass
     return hbm, hbm_src, fp64, fp64_src

@@ -58,13 +58,26 @@ class Rk4Reference:
         return (1.0 - w) * self.table[lo] + w * self.table[lo + 1]
 
 
-def reference_for(name: str, ctx=None):
-    """The named problem's accuracy reference t -> y(t) (problems.cpp:116-190)."""
+def reference_for(name: str, ctx=None, grid_steps: int = 0):
+    """The named problem's accuracy reference t -> y(t) (problems.cpp:116-190).
+
+    The reference integrates its RK4 table with 32768 steps whatever the
+    grid (problems.cpp:112), so RMSE on grids finer than the table measures
+    the table's own interpolation and truncation error (SURVEY.md §8(f)
+    item 3).  Given the grid's step count, the table here is refined to a
+    power-of-two multiple of it (>= 32768 steps): every grid node is then a
+    table node (no interpolation), and the step-halving check bounds the
+    table's error at the finer step."""
     if name == "logistic":
         y0 = 0.01
         return lambda t: np.array([y0 / (y0 + (1.0 - y0) * math.exp(-t))])
     ivp = problem_by_name(name)
-    ref = Rk4Reference(ivp, ivp.t_end / REFERENCE_STEPS, ctx)
+    steps = REFERENCE_STEPS
+    if grid_steps > REFERENCE_STEPS:
+        steps = grid_steps
+    elif grid_steps > 0:
+        steps = grid_steps * max(1, REFERENCE_STEPS // grid_steps)
+    ref = Rk4Reference(ivp, ivp.t_end / steps, ctx)
     return ref.at
 
 

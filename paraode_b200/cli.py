@@ -167,7 +167,7 @@ def cmd_benchmark(a) -> int:
     records = []
     for pname in a.problems:
         prob = _problem(pname)
-        ref = reference_for(pname)
+        refs = {}  # per grid size: a table whose nodes include the grid's (accuracy.reference_for)
         for mname in a.methods:
             run = _solver(mname)
             for nu in nus:
@@ -186,8 +186,10 @@ def cmd_benchmark(a) -> int:
                             rep = run(prob, prior, grid, P.IeksConfig())
                             if r > 0:
                                 times.append(time.perf_counter() - t0)
+                        if n not in refs:
+                            refs[n] = reference_for(pname, grid_steps=n)
                         rec.update(runtime_seconds=statistics.median(times),
-                                   rmse=rmse(rep.solution_means, ref, grid), iterations=rep.iterations,
+                                   rmse=rmse(rep.solution_means, refs[n], grid), iterations=rep.iterations,
                                    sigma_hat=rep.sigma_hat, converged=bool(rep.converged),
                                    combine_invocations=rep.combine_invocations,
                                    sequential_depth=rep.sequential_depth)

@@ -128,3 +128,42 @@ def test_benchmark_rk4_reference_accuracy(tmp_path):
 def test_compare_validates_agreement():  # test_cli.cpp:167-170
     assert cli.main(["compare", "--problems", "logistic"]) == 0
     assert cli.main(["compare", "--problems", "logistic", "--tolerance", "0"]) == 1
+
+
+def _rk4_numpy(f, y0, t_end, steps):
+    """Classical RK4 (an independent host restatement of problems.cpp:11-27)."""
+    y = np.array(y0, dtype=np.float64)
+    h = t_end / steps
+    out = [y.copy()]
+    for _ in range(steps):
+        k1 = f(y)
+        k2 = f(y + 0.5 * h * k1)
+        k3 = f(y + 0.5 * h * k2)
+        k4 = f(y + h * k3)
+        y = y + (h / 6.0) * (((k1 + 2.0 * k2) + 2.0 * k3) + k4)
+        out.append(y.copy())
+    return np.array(out)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["fhn", "vanderpol", "rigidbody"])
+def test_gpu_rk4_table_matches_independent_rk4(name):
+    """pode_rk4_table (k_rk4) against an independent numpy RK4 on the same
+    steps, and the refined reference of the benchmark harness: at a fine
+    grid the RMSE is no longer floored by the 32768-step table."""
+    import paraode_b200 as P
+    from paraode_b200.accuracy import reference_for, rk4_table
+    fields = {
+        "fhn": lambda y: np.array([3.0 * ((y[0] - y[0] ** 3 / 3.0) + y[1]), ((y[0] - 0.2) + 0.2 * y[1]) * (-1.0 / 3.0)]),
+        "vanderpol": lambda y: np.array([y[1], 1.0 * ((1.0 - y[0] * y[0]) * y[1] - y[0])]),
+        "rigidbody": lambda y: np.array([-2.0 * (y[1] * y[2]), 1.25 * (y[0] * y[2]), -0.5 * (y[0] * y[1])]),
+    }
+    prob = P.problem_by_name(name)
+    got = rk4_table(prob, 4096)
+    want = _rk4_numpy(fields[name], prob.y0, prob.t_end, 4096)
+    assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.abs(want).max())
+    n = 2 ** 16  # a grid finer than the reference's fixed 32768-step table
+    grid = P.uniform_grid(prob.t_end, n)
+    ref = reference_for(name, grid_steps=n)
+    table = rk4_table(prob, 2 * n)[::2]  # Rk4Reference keeps the step-halved table
+    assert np.array_equal(np.array([ref(float(t)) for t in grid[:: n // 64]]), table[:: n // 64])
