@@ -71,6 +71,29 @@ struct BigArgs {
   const double* m0;    // T_0^-1 mu_0
   double* ws;          // per-chunk workspace
   int64_t ws_stride;   // doubles per chunk
+  long long* phases;   // PODE_BIG_PHASES: per-phase clock64 totals of CTA 0 (debug; nullptr = off)
+};
+
+// Phase timer of CTA 0, thread 0 (between CTA barriers, so a phase's time
+// is the CTA's).
+struct PhaseClock {
+  long long* out = nullptr;
+  long long t = 0;
+  __device__ explicit PhaseClock(long long* o) {
+#ifdef __CUDA_ARCH__
+    out = (blockIdx.x == 0 && threadIdx.x == 0) ? o : nullptr;
+    t = clock64();
+#endif
+  }
+  __device__ void mark(int i) {
+#ifdef __CUDA_ARCH__
+    if (out) {
+      const long long n = clock64();
+      out[i] += n - t;
+      t = n;
+    }
+#endif
+  }
 };
 
 template <int D, int d>
@@ -134,6 +157,34 @@ struct Big {
         acc += M[r * D + j];
         Y[r * D + j] = acc;
         Y[j * D + r] = acc;
+      }
+    }
+    __syncthreads();
+  }
+  // strided forms on shared-memory operands (stride ls): Y = X Phi^T, and
+  // Pm = Phi Y + M (lower, mirrored) into both sy (smem) and Pg (global, D)
+  __device__ static void phi_cols_s(const Sm& s, const double* X, int lx, double* Y, int ly) {
+    for (int r = threadIdx.x >> 5; r < D; r += kBW)
+      for (int j = threadIdx.x & 31; j < D; j += 32) {
+        const int blk = j / B, a = j - blk * B;
+        double acc = 0.0;
+        for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[r * lx + blk * B + i], acc);
+        Y[r * ly + j] = acc;
+      }
+    __syncthreads();
+  }
+  __device__ static void phi_rows_sym_s(const Sm& s, const double* X, int lx, const double* M, double* Pg,
+                                        double* Y, int ly) {
+    for (int r = threadIdx.x >> 5; r < D; r += kBW) {
+      const int blk = r / B, a = r - blk * B;
+      for (int j = threadIdx.x & 31; j <= r; j += 32) {
+        double acc = 0.0;
+        for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[(blk * B + i) * lx + j], acc);
+        acc += M[r * D + j];
+        Y[r * ly + j] = acc;
+        Y[j * ly + r] = acc;
+        Pg[r * D + j] = acc;
+        Pg[j * D + r] = acc;
       }
     }
     __syncthreads();
@@ -254,12 +305,12 @@ struct Big {
     __syncthreads();
   }
   // HX (d x D) = H_bar X; H_bar row i = t1 e_{iB+1} - t0 sum_c jac[i][c] e_{cB}
-  __device__ static void h_rows(const Sm& s, const double* X, double* HX) {
+  __device__ static void h_rows(const Sm& s, const double* X, double* HX, int lx = D) {
     const double t0 = s.tn[0], t1 = s.tn[1];
     for (int i = threadIdx.x >> 5; i < d; i += kBW)
       for (int j = threadIdx.x & 31; j < D; j += 32) {
-        double acc = (1.0 * t1) * X[(i * B + 1) * D + j];
-        for (int c = 0; c < d; ++c) acc = fma((-s.jac[i * d + c]) * t0, X[(c * B) * D + j], acc);
+        double acc = (1.0 * t1) * X[(i * B + 1) * lx + j];
+        for (int c = 0; c < d; ++c) acc = fma((-s.jac[i * d + c]) * t0, X[(c * B) * lx + j], acc);
         HX[i * D + j] = acc;
       }
     __syncthreads();
@@ -292,7 +343,9 @@ struct Big {
 // matrix and D + 1 right-hand sides).
 template <int D>
 constexpr size_t big_smem_bytes(bool) {
-  return sizeof(double) * (size_t(D) * (D + 1) + size_t(D) * (D + 2));
+  // two D x D smem matrices (stride smem_ld), and at least D (D + 1) + D (D + 2)
+  // for trtri_lower / lu_solve
+  return sizeof(double) * 2 * size_t(D) * (smem_ld(D) > D + 2 ? smem_ld(D) : D + 2);
 }
 
 // Per-chunk workspace slots (doubles), see the kernels.
@@ -309,9 +362,10 @@ struct Slots {
 // R = 0, sequential.cpp:41-67): from Pm (predicted) produce W = S^-1 H Pm
 // (d x D) and Sinv (d x d); P+ = Pm - W^T W, K = W^T S^-1.
 template <int D, int d>
-__device__ bool cov_update_parts(StepSm<D, d>& s, const double* Pm, double* HP, double* Sd, double* Sinv, double* W) {
+__device__ bool cov_update_parts(StepSm<D, d>& s, const double* Pm, double* HP, double* Sd, double* Sinv, double* W,
+                                 int lp = D) {
   using G = Big<D, d>;
-  G::h_rows(s, Pm, HP);          // H Pm
+  G::h_rows(s, Pm, HP, lp);      // H Pm (Pm: stride lp, global or shared)
   G::h_cols(s, d, HP, Sd);       // S S^T = H Pm H^T
   const bool sing = potrf(d, Sd, d, s.red);
   trtri_lower(d, Sd, d, Sinv, d);
@@ -455,54 +509,75 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_down(BigArgs a, const double* p
   const int64_t c = blockIdx.x;
   const int64_t s0 = c * a.L, e = min(a.N, s0 + a.L);
   double* w = a.ws + c * a.ws_stride;
-  double *P = w, *Y = w + S::DD, *Pm = w + 2 * S::DD, *Lc = w + 3 * S::DD, *Li = w + 4 * S::DD,
-         *Z = w + 5 * S::DD, *EA = w + 6 * S::DD, *EAn = w + 7 * S::DD;
+  double *Pm = w + 2 * S::DD, *EA = w + 6 * S::DD, *EAn = w + 7 * S::DD;
   double* sm = w + S::kMats * S::DD;
   double *HP = sm, *W = sm + S::dD;
   double *Sd = sm + 6 * S::dD, *Sinv = Sd + d * d, *m = Sinv + d * d, *mm = m + D, *gk = mm + D, *gA = gk + D,
          *z = gA + D, *zb = z + d;
+  // Two shared-memory D x D matrices carry the step: P (filtered covariance)
+  // lives in b2 between steps.  Per step: b1 <- Y = P phi^T; b2 <- Pm =
+  // phi Y + Q Q^T (also to global); b2 <- L (Pm = L L^T); b1 <- Y L^-T L^-1
+  // = E; b2 <- Pm (from global) for the measurement update; b2 <- P+.
+  constexpr int ls = smem_ld(D);
+  double* b1 = dyn_smem();
+  double* b2 = b1 + D * ls;
   const double* pin = (c == 0) ? (first ? nullptr : carry) : prefix + (c - 1) * (S::DD + D);
-  for (int idx = threadIdx.x; idx < D * D; idx += kBT) P[idx] = pin ? pin[D + idx] : 0.0;
+  if (pin) {
+    stage(D, D, pin + D, D, b2, ls);
+  } else {
+    for (int idx = threadIdx.x; idx < D * D; idx += kBT) b2[(idx / D) * ls + idx % D] = 0.0;
+  }
   for (int r = threadIdx.x; r < D; r += kBT) m[r] = pin ? pin[r] : a.m0[r];
   __syncthreads();
   bool bad_sing = false;
   int64_t bad_lin = -1;
   double inn = 0.0;
   for (int64_t k = s0; k < e; ++k) {
+    PhaseClock pc(a.phases);
     G::step_consts(s, a.grid, k);
-    if constexpr (kFinal) copy(D * D, P, pf + k * S::DD);
-    G::phi_cols(s, P, Y);   // Y = P phi^T
-    G::phi_rows_sym(s, Y, a.qq, Pm);  // Pm = phi P phi^T + Q Q^T
-    copy(D * D, Pm, Lc);
-    bad_sing |= potrf(D, Lc, D, s.red);                                // Pm = L L^T
-    trtri_lower(D, Lc, D, Li, D);                                      // L^-1
-    gemm<false, true>(D, D, D, 1.0, Y, D, Li, D, 0.0, Z, D);           // Y L^-T
+    if constexpr (kFinal) stage(D, D, b2, ls, pf + k * S::DD, D);
+    pc.mark(0);
+    G::phi_cols_s(s, b2, ls, b1, ls);
+    G::phi_rows_sym_s(s, b1, ls, a.qq, Pm, b2, ls);
+    pc.mark(1);
+    bad_sing |= potrf_smem(D, b2, ls, s.red);
+    pc.mark(2);
+    trsm_right_lower_t(D, D, b2, ls, b1, ls);
+    pc.mark(3);
+    trsm_right_lower_n(D, D, b2, ls, b1, ls);
+    pc.mark(4);
     double* Ek = E_out + k * S::DD;
-    gemm<false, false>(D, D, D, 1.0, Z, D, Li, D, 0.0, Ek, D);         // E = Y L^-T L^-1
+    stage(D, D, b1, ls, Ek, D);
+    pc.mark(5);
     G::phi_vec(s, m, mm);                                              // m- = phi m
-    gemv<false>(D, D, -1.0, Ek, D, mm, 0.0, gk);                       // -E m-
+    gemv<false>(D, D, -1.0, b1, ls, mm, 0.0, gk);                      // -E m-
     for (int r = threadIdx.x; r < D; r += kBT) {
       gk[r] += m[r];                                                   // g = m - E phi m
       g_out[k * D + r] = gk[r];
     }
     __syncthreads();
+    pc.mark(6);
     if constexpr (!kFinal) {
       // backward aggregate (E, g) <- (E E_k, E g_k + g) (⊗_s on means)
       if (k == s0) {
-        copy(D * D, Ek, EA);
+        stage(D, D, b1, ls, EA, D);
         copy(D, gk, gA);
       } else {
         gemv<false>(D, D, 1.0, EA, D, gk, 1.0, gA);
-        gemm<false, false>(D, D, D, 1.0, EA, D, Ek, D, 0.0, EAn, D);
+        gemm_core<false>(D, D, D, 1.0, EA, D, b1, ls, 0.0, EAn, D);
         double* t = EA;
         EA = EAn;
         EAn = t;
       }
     }
+    pc.mark(7);
     // measurement update at node k+1
     G::linearize(s, a, k + 1);
     if (!s.finite && bad_lin < 0) bad_lin = k + 1;
-    bad_sing |= cov_update_parts<D, d>(s, Pm, HP, Sd, Sinv, W);
+    stage(D, D, Pm, D, b2, ls);
+    pc.mark(8);
+    bad_sing |= cov_update_parts<D, d>(s, b2, HP, Sd, Sinv, W, ls);  // scratch: b1
+    pc.mark(9);
     G::h_vec(s, mm, z);                             // H m- - offset
     gemv<false>(d, d, 1.0, Sinv, d, z, 0.0, zb);    // S^-1 z
     if constexpr (kFinal) {
@@ -511,14 +586,12 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_down(BigArgs a, const double* p
     }
     copy(D, mm, m);
     gemv<true>(D, d, -1.0, W, D, zb, 1.0, m);       // m+ = m- - W^T S^-1 z
-    gemm<true, false>(D, D, d, -1.0, W, D, W, D, 1.0, Pm, D);  // P+ = Pm - W^T W
-    double* t = P;
-    P = Pm;
-    Pm = t;
+    gemm<true, false>(D, D, d, -1.0, W, D, W, D, 1.0, b2, ls);  // P+ = Pm - W^T W (staging: b1)
+    pc.mark(10);
   }
   if (e == a.N) {  // terminal node N: E = 0, g = m_f(N)
     copy(D, m, g_term);
-    if constexpr (kFinal) copy(D * D, P, pterm);
+    if constexpr (kFinal) stage(D, D, b2, ls, pterm, D);
   }
   if constexpr (!kFinal) {
     const bool term = e == a.N && last;

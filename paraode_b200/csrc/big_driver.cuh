@@ -96,6 +96,11 @@ struct BigEngine {
     a.m0 = s.init_m;
     a.ws = wsp;
     a.ws_stride = S::kStride;
+    const bool phases = std::getenv("PODE_BIG_PHASES") != nullptr;
+    if (phases) {
+      a.phases = ws.arr<long long>("big_phases", 16);
+      cuda_check(cudaMemsetAsync(a.phases, 0, sizeof(long long) * 16, st), "phases");
+    }
     const unsigned th = big::kBT;
 
     grp::k_eta_fill_rows<D><<<grid1(n1 * D), kRedThreads, 0, st>>>(s.mu0, N, eta_a);
@@ -148,6 +153,14 @@ struct BigEngine {
       }
     }
     res.iterations = it;
+    if (phases) {  // debug: pass-C phase split of CTA 0 (clock64 cycles, all iterations)
+      long long h[16];
+      cuda_check(cudaMemcpy(h, a.phases, sizeof(h), cudaMemcpyDeviceToHost), "phases");
+      std::fprintf(stderr, "[pode] big pass C phases (Mcycles, CTA 0):");
+      for (int i = 0; i < 11; ++i) std::fprintf(stderr, " %d:%.2f", i, h[i] * 1e-6);
+      std::fprintf(stderr, "\n");
+      a.phases = nullptr;
+    }
     // finalize at the final linearisation point (eta_b) with the newest
     // trajectory (eta_a); the last pass-B prefixes are for that point
     double* pf = ws.arr<double>("big_pf", size_t(N) * DD + DD);

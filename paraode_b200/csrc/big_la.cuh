@@ -38,26 +38,61 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b,
 // read).  op(X) = X^T when TX.  M, K any; N <= 8 * kNT.  op(B) is staged in
 // shared memory (dyn_smem: >= K (N + 1) doubles, odd row stride: conflict-free
 // fragment reads); each warp owns 8-row blocks of C and sweeps all N/8
-// column tiles with the A fragment in registers (one DMMA m8n8k4 per tile
-// per k-step, the next A fragment loaded ahead).  C must not alias A or B.
+// column tiles with its A panel in registers (one DMMA m8n8k4 per tile
+// per k-step; the panel's fragments all loaded up front).  C must not alias A or B.
 constexpr int kNT = 16;  // N <= 128
+
+// Row stride of a shared-memory matrix with n columns: >= n and = 4 mod 16
+// doubles, so the 8 x 4 DMMA fragment reads (8 rows x 4 columns, or 4 rows x
+// 8 columns) of a half-warp hit 16 distinct 8-byte bank pairs.
+__host__ __device__ constexpr int smem_ld(int n) { return ((n + 11) / 16) * 16 + 4; }
+
+// The DMMA core with op(B) already in shared memory (Bs, K x N, stride ldbs).
+template <bool TA>
+__device__ void gemm_core(int M, int N, int K, double alpha, const double* A, int lda, const double* sm, int ldb_s,
+                          double beta, double* C, int ldc);
+
 template <bool TA, bool TB>
 __device__ void gemm(int M, int N, int K, double alpha, const double* A, int lda, const double* B, int ldb,
                      double beta, double* C, int ldc) {
   double* sm = dyn_smem();
-  const int ldb_s = N + 1;
-  for (int idx = threadIdx.x; idx < K * N; idx += kBT) {
-    int k, n;
-    if (TB) {  // B stored N x K: read along k
-      n = idx / K;
-      k = idx - n * K;
-    } else {
-      k = idx / N;
-      n = idx - k * N;
+  const int ldb_s = smem_ld(N);
+  for (int base = threadIdx.x; base < K * N; base += 4 * kBT) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // 4 loads in flight per thread
+      const int idx = base + u * kBT;
+      if (idx < K * N) {
+        if (TB) {  // B stored N x K: read along k
+          const int n = idx / K, k = idx - n * K;
+          v[u] = B[n * ldb + k];
+        } else {
+          const int k = idx / N, n = idx - k * N;
+          v[u] = B[k * ldb + n];
+        }
+      }
     }
-    sm[k * ldb_s + n] = TB ? B[n * ldb + k] : B[k * ldb + n];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = base + u * kBT;
+      if (idx < K * N) {
+        if (TB) {
+          const int n = idx / K, k = idx - n * K;
+          sm[k * ldb_s + n] = v[u];
+        } else {
+          const int k = idx / N, n = idx - k * N;
+          sm[k * ldb_s + n] = v[u];
+        }
+      }
+    }
   }
   __syncthreads();
+  gemm_core<TA>(M, N, K, alpha, A, lda, sm, ldb_s, beta, C, ldc);
+}
+
+template <bool TA>
+__device__ void gemm_core(int M, int N, int K, double alpha, const double* A, int lda, const double* sm, int ldb_s,
+                          double beta, double* C, int ldc) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gr = lane >> 2, tg = lane & 3;
   const int nt = (N + 7) / 8;
@@ -69,20 +104,27 @@ __device__ void gemm(int M, int N, int K, double alpha, const double* A, int lda
     auto lda_at = [&](int k) -> double {
       return (ar < M && k < K) ? (TA ? A[k * lda + ar] : A[ar * lda + k]) : 0.0;
     };
-    double a = lda_at(tg);
-    for (int k0 = 0; k0 < K; k0 += 4) {
-      const double an = lda_at(k0 + 4 + tg);  // next fragment in flight
-      const int kb = k0 + tg;
-      const bool kin = kb < K;
+    // the warp's whole 8 x 112 A panel in registers first (28 fragments in
+    // flight), then 28 k-steps of nt independent DMMA chains
+    for (int kb0 = 0; kb0 < K; kb0 += 112) {
+      double af[28];
 #pragma unroll
-      for (int t = 0; t < kNT; ++t) {
-        if (t < nt) {
-          const int col = t * 8 + gr;
-          const double b = (kin && col < N) ? sm[kb * ldb_s + col] : 0.0;
-          dmma(acc[t][0], acc[t][1], a, b, acc[t][0], acc[t][1]);
+      for (int q = 0; q < 28; ++q) af[q] = lda_at(kb0 + q * 4 + tg);
+#pragma unroll
+      for (int q = 0; q < 28; ++q) {
+        const int kb = kb0 + q * 4 + tg;
+        if (kb0 + q * 4 < K) {
+          const bool kin = kb < K;
+#pragma unroll
+          for (int t = 0; t < kNT; ++t) {
+            if (t < nt) {
+              const int col = t * 8 + gr;
+              const double b = (kin && col < N) ? sm[kb * ldb_s + col] : 0.0;
+              dmma(acc[t][0], acc[t][1], af[q], b, acc[t][0], acc[t][1]);
+            }
+          }
         }
       }
-      a = an;
     }
     const int r = m0 + gr;
     if (r < M) {
@@ -117,20 +159,33 @@ __device__ void gemv(int M, int K, double alpha, const double* A, int lda, const
     }
   } else {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = warp; i < M; i += kBW) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // independent chains: loads in flight
-      int k = lane;
-      for (; k + 96 < K; k += 128) {
-        a0 = fma(A[i * lda + k], x[k], a0);
-        a1 = fma(A[i * lda + k + 32], x[k + 32], a1);
-        a2 = fma(A[i * lda + k + 64], x[k + 64], a2);
-        a3 = fma(A[i * lda + k + 96], x[k + 96], a3);
-      }
-      for (; k < K; k += 32) a0 = fma(A[i * lda + k], x[k], a0);
-      double acc = (a0 + a1) + (a2 + a3);
+    constexpr int R = 4, C = 4;  // rows per warp pass, 32-column chunks per load batch (K <= 128 in one batch)
+    for (int i0 = warp * R; i0 < M; i0 += kBW * R) {
+      double acc[R];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) y[i] = (beta == 0.0) ? alpha * acc : fma(alpha, acc, beta * y[i]);
+      for (int u = 0; u < R; ++u) acc[u] = 0.0;
+      for (int kb = 0; kb < K; kb += 32 * C) {
+        double v[R][C];
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+#pragma unroll
+          for (int q = 0; q < C; ++q) {
+            const int k = kb + q * 32 + lane, i = i0 + u;
+            v[u][q] = (i < M && k < K) ? A[i * lda + k] * x[k] : 0.0;
+          }
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+#pragma unroll
+          for (int q = 0; q < C; ++q) acc[u] += v[u][q];
+      }
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        double t = acc[u];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        const int i = i0 + u;
+        if (lane == 0 && i < M) y[i] = (beta == 0.0) ? alpha * t : fma(alpha, t, beta * y[i]);
+      }
     }
   }
   __syncthreads();
@@ -138,6 +193,27 @@ __device__ void gemv(int M, int K, double alpha, const double* A, int lda, const
 
 __device__ __forceinline__ void copy(int n, const double* src, double* dst) {
   for (int i = threadIdx.x; i < n; i += kBT) dst[i] = src[i];
+  __syncthreads();
+}
+
+// dst (rows x cols, stride ldd) <- src (stride lds), 8 loads in flight per
+// thread (generic pointers: without batching every load waits on the
+// previous store).
+__device__ __forceinline__ void stage(int rows, int cols, const double* src, int lds, double* dst, int ldd) {
+  const int n = rows * cols;
+  for (int base = threadIdx.x; base < n; base += 8 * kBT) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * kBT;
+      v[u] = idx < n ? src[(idx / cols) * lds + idx % cols] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * kBT;
+      if (idx < n) dst[(idx / cols) * ldd + idx % cols] = v[u];
+    }
+  }
   __syncthreads();
 }
 
@@ -326,5 +402,195 @@ __device__ void lu_solve(int n, double* A, int lda, int m, double* X, int ldx) {
   __syncthreads();
 }
 
+
+// ------------------------------------------------ blocked, smem-resident ---
+// The column-serial factorisations above pay one CTA barrier and one pass of
+// shared-memory latency per column.  The blocked forms below work on
+// matrices already staged in shared memory (stride ls), 8 columns per panel:
+// the panel is factored column by column on its 8 columns only, the trailing
+// update is a DMMA rank-8 product.
+
+// In-place lower Cholesky of the n x n SPD matrix in shared memory (upper
+// part undefined on return).  Panel columns are kept unscaled while the
+// panel factors (A <- A - a_j a_j^T / d_j), then scaled by 1/sqrt(d_j).
+// Returns true (CTA-uniform) on a non-positive pivot or |L_jj| <= 1e-13 max.
+__device__ bool potrf_smem(int n, double* sa, int ls, double* red) {
+  __shared__ double s_piv[128];     // pivots d_j
+  __shared__ double s_col[2][8];    // column j of the diagonal block (double-buffered)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gr = lane >> 2, tg = lane & 3;
+  bool bad = false;
+  for (int jb = 0; jb < n; jb += 8) {
+    const int w = min(8, n - jb);
+    // panel: thread t owns row jb + t (columns jb..jb+w-1 in registers)
+    const int t = threadIdx.x, i = jb + t;
+    const bool own = i < n;
+    double r[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) r[c] = (own && c < w) ? sa[i * ls + jb + c] : 0.0;
+    if (t < w) s_col[0][t] = r[0];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (c < w) {
+        const double* col = s_col[c & 1];
+        const double dj = col[c];  // a_jj (updated), j = jb + c
+        const double inv = dj > 0.0 ? 1.0 / dj : 0.0;
+        bad |= !(dj > 0.0);
+        if (t == 0) s_piv[jb + c] = dj;
+        // a_ik -= a_ij a_kj / d_j for the panel columns k > j (rows i > j)
+        const double lij = r[c] * inv;
+#pragma unroll
+        for (int c2 = c + 1; c2 < 8; ++c2)
+          if (c2 < w && t > c) r[c2] = fma(-lij, col[c2], r[c2]);
+        if (c + 1 < w && t < w) s_col[(c + 1) & 1][t] = r[c + 1];
+        __syncthreads();
+      }
+    }
+    // scale: L_ij = a_ij / sqrt(d_j) on and below the diagonal
+    if (own) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < w && c <= t) {
+          const double dj = s_piv[jb + c];
+          sa[i * ls + jb + c] = dj > 0.0 ? r[c] * rsqrt(dj) : 0.0;
+        }
+    }
+    __syncthreads();
+    // trailing update A22 -= L21 L21^T (lower tiles), rank w, on DMMA
+    const int r0b = jb + w, M = n - r0b;
+    if (M > 0) {
+      const int tiles = (M + 7) / 8;
+      int ti = 0, base = 0;  // tile (ti, tj), tj <= ti, flat index q = base + tj
+      for (int q = warp; q < tiles * (tiles + 1) / 2; q += kBW) {
+        while (q >= base + ti + 1) base += ++ti;
+        const int tj = q - base;
+        const int rr = r0b + ti * 8 + gr, cc = r0b + tj * 8 + 2 * tg;
+        double c0 = (rr < n && cc < n) ? sa[rr * ls + cc] : 0.0;
+        double c1 = (rr < n && cc + 1 < n) ? sa[rr * ls + cc + 1] : 0.0;
+        const int rb = r0b + tj * 8 + gr;  // B column (L21 row) for this lane
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 4) {
+          if (kk < w) {
+            const int k = jb + kk + tg;
+            const double a = (rr < n && kk + tg < w) ? -sa[rr * ls + k] : 0.0;
+            const double b = (rb < n && kk + tg < w) ? sa[rb * ls + k] : 0.0;
+            dmma(c0, c1, a, b, c0, c1);
+          }
+        }
+        if (rr < n && cc < n) sa[rr * ls + cc] = c0;
+        if (rr < n && cc + 1 < n) sa[rr * ls + cc + 1] = c1;
+      }
+      __syncthreads();
+    }
+  }
+  double dmax = 0.0;
+  for (int i = threadIdx.x; i < n; i += kBT) dmax = fmax(dmax, fabs(sa[i * ls + i]));
+  const double mx = block_max(dmax, red);
+  double mine = bad ? 1.0 : 0.0;
+  for (int i = threadIdx.x; i < n; i += kBT) mine = fmax(mine, fabs(sa[i * ls + i]) <= 1e-13 * mx ? 1.0 : 0.0);
+  return block_max(mine, red) > 0.0;
+}
+
+// X L^T = Y in place (Y: m x n in shared memory, stride ly; L: n x n lower in
+// shared memory, stride ll): column blocks of 8 left to right, the update
+// by the solved blocks on DMMA, the 8-wide diagonal solve one row per thread.
+__device__ void trsm_right_lower_t(int m, int n, const double* sl, int ll, double* sy, int ly) {
+  __shared__ double s_rd[128];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gr = lane >> 2, tg = lane & 3;
+  for (int j = threadIdx.x; j < n; j += kBT) s_rd[j] = 1.0 / sl[j * ll + j];
+  __syncthreads();
+  for (int jb = 0; jb < n; jb += 8) {
+    const int w = min(8, n - jb);
+    if (jb > 0) {  // Y[:, jb:jb+w] -= X[:, 0:jb] L[jb:jb+w, 0:jb]^T
+      for (int rt = warp; rt * 8 < m; rt += kBW) {
+        const int r = rt * 8 + gr, cc = jb + 2 * tg;
+        double c0 = (r < m && 2 * tg < w) ? sy[r * ly + cc] : 0.0;
+        double c1 = (r < m && 2 * tg + 1 < w) ? sy[r * ly + cc + 1] : 0.0;
+        const int lrow = jb + gr;  // B[k][col] = L[jb + col][k]
+        double e0 = 0.0, e1 = 0.0;  // second accumulation chain (jb is a multiple of 8)
+        for (int k0 = 0; k0 < jb; k0 += 8) {
+          const double a = r < m ? -sy[r * ly + k0 + tg] : 0.0;
+          const double b = gr < w ? sl[lrow * ll + k0 + tg] : 0.0;
+          const double a2 = r < m ? -sy[r * ly + k0 + 4 + tg] : 0.0;
+          const double b2 = gr < w ? sl[lrow * ll + k0 + 4 + tg] : 0.0;
+          dmma(c0, c1, a, b, c0, c1);
+          dmma(e0, e1, a2, b2, e0, e1);
+        }
+        c0 += e0;
+        c1 += e1;
+        if (r < m && 2 * tg < w) sy[r * ly + cc] = c0;
+        if (r < m && 2 * tg + 1 < w) sy[r * ly + cc + 1] = c1;
+      }
+      __syncthreads();
+    }
+    for (int r = threadIdx.x; r < m; r += kBT) {  // x L_bb^T = y on the block
+      double x[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < w) {
+          double acc = sy[r * ly + jb + c];
+#pragma unroll
+          for (int c2 = 0; c2 < c; ++c2) acc = fma(-x[c2], sl[(jb + c) * ll + jb + c2], acc);
+          x[c] = acc * s_rd[jb + c];
+          sy[r * ly + jb + c] = x[c];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// X L = Z in place (Z: m x n in shared memory; L lower): column blocks right
+// to left, the update by the solved blocks on DMMA.
+__device__ void trsm_right_lower_n(int m, int n, const double* sl, int ll, double* sy, int ly) {
+  __shared__ double s_rd[128];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gr = lane >> 2, tg = lane & 3;
+  for (int j = threadIdx.x; j < n; j += kBT) s_rd[j] = 1.0 / sl[j * ll + j];
+  __syncthreads();
+  const int nblk = (n + 7) / 8;
+  for (int bb = nblk - 1; bb >= 0; --bb) {
+    const int jb = bb * 8, w = min(8, n - jb), kstart = jb + w;
+    if (kstart < n) {  // Z[:, jb:jb+w] -= X[:, kstart:n] L[kstart:n, jb:jb+w]
+      for (int rt = warp; rt * 8 < m; rt += kBW) {
+        const int r = rt * 8 + gr, cc = jb + 2 * tg;
+        double c0 = (r < m && 2 * tg < w) ? sy[r * ly + cc] : 0.0;
+        double c1 = (r < m && 2 * tg + 1 < w) ? sy[r * ly + cc + 1] : 0.0;
+        double e0 = 0.0, e1 = 0.0;  // second accumulation chain
+        for (int k0 = kstart; k0 < n; k0 += 8) {
+          const int k = k0 + tg, k2 = k0 + 4 + tg;
+          const double a = (r < m && k < n) ? -sy[r * ly + k] : 0.0;
+          const double b = (k < n && gr < w) ? sl[k * ll + jb + gr] : 0.0;  // B[k][col] = L[k][jb + col]
+          const double a2 = (r < m && k2 < n) ? -sy[r * ly + k2] : 0.0;
+          const double b2 = (k2 < n && gr < w) ? sl[k2 * ll + jb + gr] : 0.0;
+          dmma(c0, c1, a, b, c0, c1);
+          dmma(e0, e1, a2, b2, e0, e1);
+        }
+        c0 += e0;
+        c1 += e1;
+        if (r < m && 2 * tg < w) sy[r * ly + cc] = c0;
+        if (r < m && 2 * tg + 1 < w) sy[r * ly + cc + 1] = c1;
+      }
+      __syncthreads();
+    }
+    for (int r = threadIdx.x; r < m; r += kBT) {  // x L_bb = z on the block
+      double x[8];
+#pragma unroll
+      for (int c = 7; c >= 0; --c) {
+        if (c < w) {
+          double acc = sy[r * ly + jb + c];
+#pragma unroll
+          for (int c2 = 7; c2 > c; --c2)
+            if (c2 < w) acc = fma(-x[c2], sl[(jb + c2) * ll + jb + c], acc);
+          x[c] = acc * s_rd[jb + c];
+          sy[r * ly + jb + c] = x[c];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
 }  // namespace big
 }  // namespace pode

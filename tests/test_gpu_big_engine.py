@@ -5,6 +5,7 @@ derivative order, covariance products L L^T and sigma_hat, under several
 chunkings (one CTA per chunk; the chunk chains of passes B / D / F3)."""
 import json
 import os
+import re
 
 import numpy as np
 import pytest
@@ -60,18 +61,35 @@ def test_pleiades_default_rule_outcome_matches_oracle():
     """The reference stopping rule on Pleiades from the constant initial
     trajectory (ieks.cpp:145-148) at N = 2^10: the oracle's seq_ieks does not
     converge within the 100-iteration budget — the Gauss-Newton iterates
-    diverge (objective ~1e19) — and neither does the GPU; the traces agree
-    while the iterates are still determined (first 3 iterations)."""
+    diverge (objective ~1e19).  The traces agree while the iterates are still
+    determined (first 3 iterations to 1e-8; tools/pleiades_chaos.py shows
+    the departure growing from ~1e-7 at iteration 8 to O(1) by iteration 16:
+    from there the iterates are decided by rounding, in the oracle as on the
+    GPU).  Outcome parity is therefore "no convergence": the GPU either
+    exhausts the budget like the oracle, or its rounding-decided iterates hit
+    the reference's singular-factor test (linalg.cpp:54-62) after the
+    departure point — never a convergence and never an error while the
+    iterates are determined."""
     path = os.path.join(GOLDEN, "pleiades_q3_n10_seq.npz")
     if not os.path.exists(path):
         pytest.skip("fixture not generated")
     z = np.load(path)
     meta = json.loads(str(z["meta"]))
-    conv = gpu_solve(P, meta)
+    assert not meta["converged"] and meta["iterations"] == meta["max_iterations"]
+    early = gpu_solve(P, meta, max_iterations=3, **NEVER)
+    assert np.allclose(early.objective_trace, z["objective_trace"][:3], rtol=1e-8)
+    try:
+        conv = gpu_solve(P, meta)
+    except P.SingularFactorError as e:
+        m = re.search(r"iteration (\d+)", str(e))
+        assert m and int(m.group(1)) > 16, str(e)
+        print(f"pleiades q3 N=2^10 default rule: GPU singular factor after the departure ({e}); "
+              f"oracle {meta['iterations']} its conv={meta['converged']}")
+        return
     print(f"pleiades q3 N=2^10 default rule: GPU {conv.iterations} its conv={conv.converged}; "
           f"oracle {meta['iterations']} its conv={meta['converged']}; final objective GPU "
           f"{conv.objective_trace[-1]:.3e}, oracle {z['objective_trace'][-1]:.3e}")
-    assert conv.converged == meta["converged"] and conv.iterations == meta["iterations"]
+    assert not conv.converged and conv.iterations == meta["iterations"]
     assert np.allclose(conv.objective_trace[:3], z["objective_trace"][:3], rtol=1e-8)
 
 
