@@ -133,83 +133,118 @@ struct Big {
     }
     __syncthreads();
   }
-  // Y = Phi X (rows), Y != X
-  __device__ static void phi_rows(const Sm& s, const double* X, double* Y) {
-    for (int r = threadIdx.x >> 5; r < D; r += kBW) {
-      const int blk = r / B, a = r - blk * B;
-      for (int j = threadIdx.x & 31; j < D; j += 32) {
-        double acc = 0.0;
-        for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[(blk * B + i) * D + j], acc);
-        Y[r * D + j] = acc;
+  // The transition acts blockwise (B x B upper-triangular bin per state
+  // component), so every product below is a set of independent block tasks;
+  // each thread keeps kU tasks (kU * B loads) in flight.  Strides lx / ly
+  // address global or shared operands alike.  Y != X throughout.
+  static constexpr int kU = 4;
+  // Y = Phi X (rows): task (blk, column j)
+  __device__ static void phi_rows(const Sm& s, const double* X, int lx, double* Y, int ly) {
+    constexpr int T = d * D;
+    for (int base = threadIdx.x; base < T; base += kU * kBT) {
+      double x[kU][B];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int t = base + u * kBT, blk = t / D, j = t - blk * D;
+#pragma unroll
+        for (int i = 0; i < B; ++i) x[u][i] = t < T ? X[(blk * B + i) * lx + j] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int t = base + u * kBT, blk = t / D, j = t - blk * D;
+        if (t < T) {
+#pragma unroll
+          for (int a = 0; a < B; ++a) {
+            double acc = 0.0;
+#pragma unroll
+            for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], x[u][i], acc);
+            Y[(blk * B + a) * ly + j] = acc;
+          }
+        }
       }
     }
     __syncthreads();
   }
-  // Y = Phi X + M on and below the diagonal, mirrored above: the predicted
-  // covariance phi (P phi^T) + Q Q^T, exactly symmetric (the two triangles
-  // of phi P phi^T would otherwise differ by the association order).
-  __device__ static void phi_rows_sym(const Sm& s, const double* X, const double* M, double* Y) {
-    for (int r = threadIdx.x >> 5; r < D; r += kBW) {
-      const int blk = r / B, a = r - blk * B;
-      for (int j = threadIdx.x & 31; j <= r; j += 32) {
-        double acc = 0.0;
-        for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[(blk * B + i) * D + j], acc);
-        acc += M[r * D + j];
-        Y[r * D + j] = acc;
-        Y[j * D + r] = acc;
+  // Y = Phi X + M on and below the diagonal, mirrored above (M: D x D,
+  // stride D): the predicted covariance phi (P phi^T) + Q Q^T, exactly
+  // symmetric (the two triangles of phi P phi^T would otherwise differ by
+  // the association order); also written to Pg (stride D) when given.
+  __device__ static void phi_rows_sym(const Sm& s, const double* X, int lx, const double* M, double* Y, int ly,
+                                      double* Pg = nullptr) {
+    constexpr int T = d * D;
+    for (int base = threadIdx.x; base < T; base += kU * kBT) {
+      double x[kU][B], mv[kU][B];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int t = base + u * kBT, blk = t / D, j = t - blk * D;
+#pragma unroll
+        for (int i = 0; i < B; ++i) {
+          const bool lo = t < T && blk * B + i >= j;
+          x[u][i] = lo ? X[(blk * B + i) * lx + j] : 0.0;
+          mv[u][i] = lo ? M[(blk * B + i) * D + j] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int t = base + u * kBT, blk = t / D, j = t - blk * D;
+#pragma unroll
+        for (int a = 0; a < B; ++a) {
+          const int r = blk * B + a;
+          if (t < T && r >= j) {
+            double acc = 0.0;
+#pragma unroll
+            for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], x[u][i], acc);
+            acc += mv[u][a];
+            Y[r * ly + j] = acc;
+            Y[j * ly + r] = acc;
+            if (Pg) {
+              Pg[r * D + j] = acc;
+              Pg[j * D + r] = acc;
+            }
+          }
+        }
       }
     }
     __syncthreads();
   }
-  // strided forms on shared-memory operands (stride ls): Y = X Phi^T, and
-  // Pm = Phi Y + M (lower, mirrored) into both sy (smem) and Pg (global, D)
-  __device__ static void phi_cols_s(const Sm& s, const double* X, int lx, double* Y, int ly) {
-    for (int r = threadIdx.x >> 5; r < D; r += kBW)
-      for (int j = threadIdx.x & 31; j < D; j += 32) {
-        const int blk = j / B, a = j - blk * B;
-        double acc = 0.0;
-        for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[r * lx + blk * B + i], acc);
-        Y[r * ly + j] = acc;
+  // Y = X Phi^T (kT) or Y = X Phi (!kT): task (row r, blk)
+  template <bool kT>
+  __device__ static void phi_colwise(const Sm& s, const double* X, int lx, double* Y, int ly) {
+    constexpr int T = D * d;
+    for (int base = threadIdx.x; base < T; base += kU * kBT) {
+      double x[kU][B];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int t = base + u * kBT, r = t / d, blk = t - r * d;
+#pragma unroll
+        for (int i = 0; i < B; ++i) x[u][i] = t < T ? X[r * lx + blk * B + i] : 0.0;
       }
-    __syncthreads();
-  }
-  __device__ static void phi_rows_sym_s(const Sm& s, const double* X, int lx, const double* M, double* Pg,
-                                        double* Y, int ly) {
-    for (int r = threadIdx.x >> 5; r < D; r += kBW) {
-      const int blk = r / B, a = r - blk * B;
-      for (int j = threadIdx.x & 31; j <= r; j += 32) {
-        double acc = 0.0;
-        for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[(blk * B + i) * lx + j], acc);
-        acc += M[r * D + j];
-        Y[r * ly + j] = acc;
-        Y[j * ly + r] = acc;
-        Pg[r * D + j] = acc;
-        Pg[j * D + r] = acc;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int t = base + u * kBT, r = t / d, blk = t - r * d;
+        if (t < T) {
+#pragma unroll
+          for (int c = 0; c < B; ++c) {
+            double acc = 0.0;
+            if (kT) {  // Y[r][blk B + c] = sum_{i >= c} bin[c][i] X[r][blk B + i]
+#pragma unroll
+              for (int i = c; i < B; ++i) acc = fma(s.bin[c][i], x[u][i], acc);
+            } else {   // Y[r][blk B + c] = sum_{i <= c} X[r][blk B + i] bin[i][c]
+#pragma unroll
+              for (int i = 0; i <= c; ++i) acc = fma(x[u][i], s.bin[i][c], acc);
+            }
+            Y[r * ly + blk * B + c] = acc;
+          }
+        }
       }
     }
     __syncthreads();
   }
-  // Y = X Phi^T (columns), Y != X
-  __device__ static void phi_cols(const Sm& s, const double* X, double* Y) {
-    for (int r = threadIdx.x >> 5; r < D; r += kBW)
-      for (int j = threadIdx.x & 31; j < D; j += 32) {
-        const int blk = j / B, a = j - blk * B;
-        double acc = 0.0;
-        for (int i = a; i < B; ++i) acc = fma(s.bin[a][i], X[r * D + blk * B + i], acc);
-        Y[r * D + j] = acc;
-      }
-    __syncthreads();
+  __device__ static void phi_cols(const Sm& s, const double* X, int lx, double* Y, int ly) {
+    phi_colwise<true>(s, X, lx, Y, ly);
   }
-  // Y = X Phi (columns), Y != X: Y[r][blk B + c] = sum_{a <= c} X[r][blk B + a] Phi[a][c]
-  __device__ static void phi_right(const Sm& s, const double* X, double* Y) {
-    for (int r = threadIdx.x >> 5; r < D; r += kBW)
-      for (int j = threadIdx.x & 31; j < D; j += 32) {
-        const int blk = j / B, cc = j - blk * B;
-        double acc = 0.0;
-        for (int aa = 0; aa <= cc; ++aa) acc = fma(X[r * D + blk * B + aa], s.bin[aa][cc], acc);
-        Y[r * D + j] = acc;
-      }
-    __syncthreads();
+  __device__ static void phi_right(const Sm& s, const double* X, int lx, double* Y, int ly) {
+    phi_colwise<false>(s, X, lx, Y, ly);
   }
   __device__ static void phi_vec(const Sm& s, const double* x, double* y) {
     for (int r = threadIdx.x; r < D; r += kBT) {
@@ -316,13 +351,25 @@ struct Big {
     __syncthreads();
   }
   // XH (n x d) = X H_bar^T for X with n rows of D
-  __device__ static void h_cols(const Sm& s, int n, const double* X, double* XH) {
+  __device__ static void h_cols(const Sm& s, int n, const double* X, double* XH, int lx = D, int lo = d) {
     const double t0 = s.tn[0], t1 = s.tn[1];
     for (int idx = threadIdx.x; idx < n * d; idx += kBT) {
       const int r = idx / d, i = idx - (idx / d) * d;
-      double acc = (1.0 * t1) * X[r * D + i * B + 1];
-      for (int c = 0; c < d; ++c) acc = fma((-s.jac[i * d + c]) * t0, X[r * D + c * B], acc);
-      XH[idx] = acc;
+      double acc = (1.0 * t1) * X[r * lx + i * B + 1];
+      for (int c = 0; c < d; ++c) acc = fma((-s.jac[i * d + c]) * t0, X[r * lx + c * B], acc);
+      XH[r * lo + i] = acc;
+    }
+    __syncthreads();
+  }
+  // HX (d x D, stride lo) = H_bar X for X in shared memory (stride lx): the
+  // Jacobian part as one DMMA product (jac x the rows cB of X), then the
+  // t1 rows iB+1
+  __device__ static void h_rows_smem(const Sm& s, const double* X, int lx, double* HX, int lo) {
+    gemm_core<false>(d, D, d, -s.tn[0], s.jac, d, X, B * lx, 0.0, HX, lo);
+    const double t1 = s.tn[1];
+    for (int idx = threadIdx.x; idx < d * D; idx += kBT) {
+      const int i = idx / D, j = idx - (idx / D) * D;
+      HX[i * lo + j] = fma(t1, X[(i * B + 1) * lx + j], HX[i * lo + j]);
     }
     __syncthreads();
   }
@@ -338,14 +385,19 @@ struct Big {
   }
 };
 
-// Dynamic shared memory of the kernels (big_la.cuh staging): two D x D
-// operands at stride D + 1 (trtri: L and its inverse; the chain's LU: the
-// matrix and D + 1 right-hand sides).
+// Dynamic shared memory of the kernels: b1 (offset 0: the staging area of
+// the big_la.cuh routines and of cov_update_parts) and b2 (a resident D x D
+// matrix, stride smem_ld(D)) after it; the chain kernels' LU needs
+// D (D + 1) + D (D + 2).
+template <int D, int d = 28>
+constexpr int b2_offset() {
+  constexpr int ls = smem_ld(D), scratch = d * smem_ld(D) + 2 * d * smem_ld(d);
+  return D * ls > scratch ? D * ls : scratch;
+}
 template <int D>
 constexpr size_t big_smem_bytes(bool) {
-  // two D x D smem matrices (stride smem_ld), and at least D (D + 1) + D (D + 2)
-  // for trtri_lower / lu_solve
-  return sizeof(double) * 2 * size_t(D) * (smem_ld(D) > D + 2 ? smem_ld(D) : D + 2);
+  constexpr size_t two = size_t(b2_offset<D>()) + size_t(D) * smem_ld(D), lu = size_t(D) * (2 * D + 3);
+  return sizeof(double) * (two > lu ? two : lu);
 }
 
 // Per-chunk workspace slots (doubles), see the kernels.
@@ -362,14 +414,20 @@ struct Slots {
 // R = 0, sequential.cpp:41-67): from Pm (predicted) produce W = S^-1 H Pm
 // (d x D) and Sinv (d x d); P+ = Pm - W^T W, K = W^T S^-1.
 template <int D, int d>
-__device__ bool cov_update_parts(StepSm<D, d>& s, const double* Pm, double* HP, double* Sd, double* Sinv, double* W,
-                                 int lp = D) {
+__device__ bool cov_update_parts(StepSm<D, d>& s, const double* Pm, int lp, double* Sinv, double* W) {
   using G = Big<D, d>;
-  G::h_rows(s, Pm, HP, lp);      // H Pm (Pm: stride lp, global or shared)
-  G::h_cols(s, d, HP, Sd);       // S S^T = H Pm H^T
-  const bool sing = potrf(d, Sd, d, s.red);
-  trtri_lower(d, Sd, d, Sinv, d);
-  gemm<false, false>(d, D, d, 1.0, Sinv, d, HP, D, 0.0, W, D);  // W = S^-1 H Pm
+  constexpr int lh = smem_ld(D), l2 = smem_ld(d);
+  double* hp = dyn_smem();         // H Pm (d x D), then W = S^-1 H Pm
+  double* ss = hp + d * lh;        // S S^T = H Pm H^T (d x d), then S
+  double* si = ss + d * l2;        // I, then S^-1
+  G::h_rows_smem(s, Pm, lp, hp, lh);
+  G::h_cols(s, d, hp, ss, lh, l2);
+  for (int idx = threadIdx.x; idx < d * d; idx += kBT) si[(idx / d) * l2 + idx % d] = (idx / d == idx % d) ? 1.0 : 0.0;
+  const bool sing = potrf_smem(d, ss, l2, s.red);  // (syncs)
+  trsm_left_lower(d, D, ss, l2, hp, lh);           // W = S^-1 H Pm
+  trsm_left_lower(d, d, ss, l2, si, l2);           // S^-1
+  stage(d, D, hp, lh, W, D);
+  stage(d, d, si, l2, Sinv, d);
   return sing;
 }
 
@@ -382,17 +440,21 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_reduce(BigArgs a, double* agg, 
   const int64_t c = blockIdx.x;
   const int64_t s0 = c * a.L, e = min(a.N, s0 + a.L);
   double* w = a.ws + c * a.ws_stride;
-  double *Am = w, *P = w + S::DD, *Lam = w + 2 * S::DD, *T1 = w + 3 * S::DD, *Pm = w + 4 * S::DD,
-         *Anew = w + 5 * S::DD;
+  double *Am = w, *Lam = w + 2 * S::DD, *Anew = w + 5 * S::DD;
   double* sm = w + S::kMats * S::DD;
-  double *HP = sm, *W = sm + S::dD, *HA = sm + 2 * S::dD, *Ub = sm + 3 * S::dD;
+  double *W = sm + S::dD, *HA = sm + 2 * S::dD, *Ub = sm + 3 * S::dD;
   double *Sd = sm + 6 * S::dD, *Sinv = Sd + d * d, *bv = Sinv + d * d, *bm = bv + D, *eta = bm + D, *u = eta + D,
          *ub = u + d;
+  // P lives in shared memory (b2) for the whole chunk; b1 is the scratch
+  // of the products (P phi^T, then the staging of the small solves).
+  constexpr int ls = smem_ld(D);
+  double* b1 = dyn_smem();
+  double* b2 = b1 + b2_offset<D, d>();
   const bool chunk0 = c == 0 && first;
   for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
     const int r = idx / D, j = idx - (idx / D) * D;
     Am[idx] = (!chunk0 && r == j) ? 1.0 : 0.0;
-    P[idx] = 0.0;
+    b2[r * ls + j] = 0.0;
     Lam[idx] = 0.0;
   }
   for (int r = threadIdx.x; r < D; r += kBT) {
@@ -404,13 +466,13 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_reduce(BigArgs a, double* agg, 
   int64_t bad_lin = -1;
   for (int64_t k = s0; k < e; ++k) {
     G::step_consts(s, a.grid, k);
-    G::phi_rows(s, Am, Anew);  // A- = phi A
-    G::phi_vec(s, bv, bm);     // b- = phi b
-    G::phi_cols(s, P, T1);     // P phi^T
-    G::phi_rows_sym(s, T1, a.qq, Pm);  // phi P phi^T + Q Q^T
+    G::phi_rows(s, Am, D, Anew, D);  // A- = phi A
+    G::phi_vec(s, bv, bm);           // b- = phi b
+    G::phi_cols(s, b2, ls, b1, ls);  // P phi^T
+    G::phi_rows_sym(s, b1, ls, a.qq, b2, ls);  // Pm = phi P phi^T + Q Q^T
     G::linearize(s, a, k + 1);
     if (!s.finite && bad_lin < 0) bad_lin = k + 1;
-    bad_sing |= cov_update_parts<D, d>(s, Pm, HP, Sd, Sinv, W);
+    bad_sing |= cov_update_parts<D, d>(s, b2, ls, Sinv, W);  // scratch: b1
     G::h_rows(s, Anew, HA);  // H A-
     G::h_vec(s, bm, u);      // H b- - offset
     gemm<false, false>(d, D, d, 1.0, Sinv, d, HA, D, 0.0, Ub, D);  // Ubar = S^-1 H A-
@@ -419,15 +481,12 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_reduce(BigArgs a, double* agg, 
     // eta -= Ubar^T ubar; Lambda += Ubar^T Ubar
     gemm<true, false>(D, D, d, -1.0, W, D, Ub, D, 1.0, Anew, D);
     gemv<true>(D, d, -1.0, W, D, ub, 1.0, bm);
-    gemm<true, false>(D, D, d, -1.0, W, D, W, D, 1.0, Pm, D);  // (P stays symmetric to rounding; the chains re-symmetrise)
+    gemm<true, false>(D, D, d, -1.0, W, D, W, D, 1.0, b2, ls);  // (P stays symmetric to rounding; the chains re-symmetrise)
     gemv<true>(D, d, -1.0, Ub, D, ub, 1.0, eta);
     gemm<true, false>(D, D, d, 1.0, Ub, D, Ub, D, 1.0, Lam, D);
-    double* t = Am;  // rotate buffers: A <- Anew, P <- Pm
+    double* t = Am;  // rotate buffers: A <- Anew
     Am = Anew;
     Anew = t;
-    t = P;
-    P = Pm;
-    Pm = t;
     copy(D, bm, bv);
   }
   if (threadIdx.x == 0) {
@@ -438,7 +497,7 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_reduce(BigArgs a, double* agg, 
   double* o = agg + c * (3 * S::DD + 2 * D);
   for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
     o[idx] = Am[idx];
-    o[S::DD + idx] = P[idx];
+    o[S::DD + idx] = b2[(idx / D) * ls + idx % D];
     o[2 * S::DD + idx] = Lam[idx];
   }
   for (int r = threadIdx.x; r < D; r += kBT) {
@@ -453,7 +512,6 @@ template <int D, int d>
 __global__ void __launch_bounds__(kBT) k_big_chain_fwd(BigArgs a, const double* agg, double* prefix, double* scratch,
                                                        int first, const double* carry) {
   using S = Slots<D, d>;
-  __shared__ double red[kBW];
   double *M = scratch, *X = scratch + S::DD, *T = X + int64_t(D) * (D + 1);
   double *m = T + S::DD, *Pc = m + D;
   const int64_t stride = 3 * S::DD + 2 * D;
@@ -511,7 +569,7 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_down(BigArgs a, const double* p
   double* w = a.ws + c * a.ws_stride;
   double *Pm = w + 2 * S::DD, *EA = w + 6 * S::DD, *EAn = w + 7 * S::DD;
   double* sm = w + S::kMats * S::DD;
-  double *HP = sm, *W = sm + S::dD;
+  double* W = sm + S::dD;
   double *Sd = sm + 6 * S::dD, *Sinv = Sd + d * d, *m = Sinv + d * d, *mm = m + D, *gk = mm + D, *gA = gk + D,
          *z = gA + D, *zb = z + d;
   // Two shared-memory D x D matrices carry the step: P (filtered covariance)
@@ -520,7 +578,7 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_down(BigArgs a, const double* p
   // = E; b2 <- Pm (from global) for the measurement update; b2 <- P+.
   constexpr int ls = smem_ld(D);
   double* b1 = dyn_smem();
-  double* b2 = b1 + D * ls;
+  double* b2 = b1 + b2_offset<D, d>();
   const double* pin = (c == 0) ? (first ? nullptr : carry) : prefix + (c - 1) * (S::DD + D);
   if (pin) {
     stage(D, D, pin + D, D, b2, ls);
@@ -537,8 +595,8 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_down(BigArgs a, const double* p
     G::step_consts(s, a.grid, k);
     if constexpr (kFinal) stage(D, D, b2, ls, pf + k * S::DD, D);
     pc.mark(0);
-    G::phi_cols_s(s, b2, ls, b1, ls);
-    G::phi_rows_sym_s(s, b1, ls, a.qq, Pm, b2, ls);
+    G::phi_cols(s, b2, ls, b1, ls);
+    G::phi_rows_sym(s, b1, ls, a.qq, b2, ls, Pm);
     pc.mark(1);
     bad_sing |= potrf_smem(D, b2, ls, s.red);
     pc.mark(2);
@@ -576,7 +634,7 @@ __global__ void __launch_bounds__(kBT) k_big_fwd_down(BigArgs a, const double* p
     if (!s.finite && bad_lin < 0) bad_lin = k + 1;
     stage(D, D, Pm, D, b2, ls);
     pc.mark(8);
-    bad_sing |= cov_update_parts<D, d>(s, b2, HP, Sd, Sinv, W, ls);  // scratch: b1
+    bad_sing |= cov_update_parts<D, d>(s, b2, ls, Sinv, W);  // scratch: b1
     pc.mark(9);
     G::h_vec(s, mm, z);                             // H m- - offset
     gemv<false>(d, d, 1.0, Sinv, d, z, 0.0, zb);    // S^-1 z
@@ -734,17 +792,15 @@ __global__ void __launch_bounds__(kBT) k_big_bwd_down(BigArgs a, const double* E
 // ------------------------------------------------- finalize (once) ---
 // M1_k = (I - E_k phi) P+_k (I - E_k phi)^T + E_k Q Q^T E_k^T: the
 // covariance of the smoothing element at node k (Joseph form).
+// M = (I - E phi) P+ (I - E phi)^T (T1, T2 scratch; all D x D, stride D).
 template <int D, int d>
-__device__ void smooth_cov(StepSm<D, d>& s, const double* Ek, const double* Pf, const double* qq, double* M1,
-                           double* T1, double* T2) {
+__device__ void smooth_joseph(StepSm<D, d>& s, const double* Ek, const double* Pf, double* T1, double* T2,
+                              double* M) {
   using G = Big<D, d>;
-  G::phi_right(s, Ek, T1);  // E phi  (phi_k = node k -> k+1)
-  for (int idx = threadIdx.x; idx < D * D; idx += kBT) T1[idx] = ((idx / D == idx % D) ? 1.0 : 0.0) - T1[idx];
-  __syncthreads();
+  G::phi_right(s, Ek, D, T1, D);  // E phi  (phi_k = node k -> k+1)
+  axpby_eye(D, -1.0, T1, 0.0, nullptr, 1.0, T1);
   gemm<false, false>(D, D, D, 1.0, T1, D, Pf, D, 0.0, T2, D);   // (I - E phi) P+
-  gemm<false, true>(D, D, D, 1.0, T2, D, T1, D, 0.0, M1, D);    // .. (I - E phi)^T
-  gemm<false, false>(D, D, D, 1.0, Ek, D, qq, D, 0.0, T2, D);   // E Q Q^T
-  gemm<false, true>(D, D, D, 1.0, T2, D, Ek, D, 1.0, M1, D);    // + E Q Q^T E^T
+  gemm<false, true>(D, D, D, 1.0, T2, D, T1, D, 0.0, M, D);     // .. (I - E phi)^T
 }
 
 // F2: per chunk the smoothing-covariance aggregate (Eagg, Lagg): P^s(s) =
@@ -769,10 +825,11 @@ __global__ void __launch_bounds__(kBT) k_big_fin_fold(BigArgs a, const double* E
   for (int64_t k = e - 1; k >= s0; --k) {
     G::step_consts(s, a.grid, k);
     const double* Ek = E_in + k * S::DD;
-    smooth_cov<D, d>(s, Ek, pf + k * S::DD, a.qq, M1, T1, T2);
-    gemm<false, false>(D, D, D, 1.0, Ek, D, LA, D, 0.0, T1, D);    // E L
-    copy(D * D, M1, LAn);
-    gemm<false, true>(D, D, D, 1.0, T1, D, Ek, D, 1.0, LAn, D);    // E L E^T + M1
+    // Lagg <- (I - E phi) P+ (I - E phi)^T + E (Q Q^T + Lagg) E^T
+    smooth_joseph<D, d>(s, Ek, pf + k * S::DD, T1, T2, LAn);
+    axpby_eye(D, 1.0, a.qq, 1.0, LA, 0.0, M1);
+    gemm<false, false>(D, D, D, 1.0, Ek, D, M1, D, 0.0, T1, D);
+    gemm<false, true>(D, D, D, 1.0, T1, D, Ek, D, 1.0, LAn, D);
     gemm<false, false>(D, D, D, 1.0, Ek, D, EA, D, 0.0, EAn, D);   // E Eagg
     double* t = EA;
     EA = EAn;
@@ -806,26 +863,27 @@ __global__ void __launch_bounds__(kBT) k_big_chain_fin(int64_t nc, const double*
   }
 }
 
-// Pivoted Cholesky of the PSD n x n A (destroyed): F (n x n, row-major)
-// with F F^T = A, F = Pi L; pivots below tol * max diag end the
-// factorisation (remaining columns zero).
-__device__ void psd_factor(int n, double* A, int lda, double* F, int ldf, int* perm, double* red) {
-  __shared__ int s_p;
-  __shared__ double s_d, s_dmax;
-  for (int idx = threadIdx.x; idx < n * n; idx += kBT) F[(idx / n) * ldf + idx % n] = 0.0;
-  for (int i = threadIdx.x; i < n; i += kBT) perm[i] = i;
-  __syncthreads();
+// Pivoted Cholesky of the PSD n x n A (destroyed): F (n x n) with F F^T = A,
+// F = Pi L; pivots below 1e-15 max diag end the factorisation (remaining
+// columns zero).  A (stride la) and F (stride lf) in shared memory: the remaining diagonal is tracked in s_dg, the pivot
+// order in perm; only the lower triangle (in pivot order) is updated.
+__device__ void psd_factor_smem(int n, double* A, int la, double* F, int lf, int* perm, double* red) {
+  __shared__ double s_dg[128];
+  __shared__ double s_d;
+  for (int idx = threadIdx.x; idx < n * n; idx += kBT) F[(idx / n) * lf + idx % n] = 0.0;
   double mloc = 0.0;
-  for (int i = threadIdx.x; i < n; i += kBT) mloc = fmax(mloc, A[i * lda + i]);
-  const double dmax0 = block_max(mloc, red);
-  if (threadIdx.x == 0) s_dmax = dmax0;
-  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += kBT) {
+    perm[i] = i;
+    s_dg[i] = A[i * la + i];
+    mloc = fmax(mloc, A[i * la + i]);
+  }
+  const double dmax0 = block_max(mloc, red);  // (syncs)
   for (int j = 0; j < n; ++j) {
-    if (threadIdx.x < 32) {  // pivot: largest remaining diagonal (positions j..n-1 in permuted order)
+    if (threadIdx.x < 32) {  // pivot: largest remaining diagonal
       double best = -1.0;
       int bi = j;
       for (int i = j + threadIdx.x; i < n; i += 32) {
-        const double v = A[perm[i] * lda + perm[i]];
+        const double v = s_dg[perm[i]];
         if (v > best) {
           best = v;
           bi = i;
@@ -841,7 +899,6 @@ __device__ void psd_factor(int n, double* A, int lda, double* F, int ldf, int* p
         }
       }
       if (threadIdx.x == 0) {
-        s_p = bi;
         s_d = best;
         const int t = perm[j];
         perm[j] = perm[bi];
@@ -849,22 +906,25 @@ __device__ void psd_factor(int n, double* A, int lda, double* F, int ldf, int* p
       }
     }
     __syncthreads();
-    if (!(s_d > 1e-15 * s_dmax)) break;  // CTA-uniform
+    if (!(s_d > 1e-15 * dmax0)) break;  // CTA-uniform
     const int pj = perm[j];
     const double l = sqrt(s_d), inv = 1.0 / l;
-    // column j of L (rows in permuted order i >= j): L[i][j] = A[pi][pj] / l
     for (int i = j + threadIdx.x; i < n; i += kBT) {
       const int pi = perm[i];
-      F[pi * ldf + j] = (i == j) ? l : A[pi * lda + pj] * inv;
+      const double v = (i == j) ? l : A[pi * la + pj] * inv;
+      F[pi * lf + j] = v;
+      if (i > j) s_dg[pi] -= v * v;
     }
     __syncthreads();
-    // Schur complement on the remaining rows/cols
+    // Schur complement, lower triangle in pivot order (ii >= kk)
     for (int ii = j + 1 + (threadIdx.x >> 5); ii < n; ii += kBW) {
       const int pi = perm[ii];
-      const double fi = F[pi * ldf + j];
-      for (int kk = j + 1 + (threadIdx.x & 31); kk < n; kk += 32) {
+      const double fi = F[pi * lf + j];
+      for (int kk = j + 1 + (threadIdx.x & 31); kk <= ii; kk += 32) {
         const int pk = perm[kk];
-        A[pi * lda + pk] = fma(-fi, F[pk * ldf + j], A[pi * lda + pk]);
+        const double v = fma(-fi, F[pk * lf + j], A[pi * la + pk]);
+        A[pi * la + pk] = v;
+        A[pk * la + pi] = v;
       }
     }
     __syncthreads();
@@ -895,17 +955,28 @@ __global__ void __launch_bounds__(kBT) k_big_fin_bwd(BigArgs a, const double* E_
   const int64_t s0 = c * a.L, e = min(a.N, s0 + a.L);
   const bool lastc = c == a.nchunks - 1;
   double* w = a.ws + c * a.ws_stride;
-  double *Pn = w, *M1 = w + S::DD, *T1 = w + 2 * S::DD, *T2 = w + 3 * S::DD, *Pk = w + 4 * S::DD,
-         *F = w + 5 * S::DD, *Ac = w + 6 * S::DD;
+  double *Pn = w, *T1 = w + 2 * S::DD, *T2 = w + 3 * S::DD, *Pk = w + 4 * S::DD, *T3 = w + 5 * S::DD;
+  constexpr int ls = smem_ld(D);
+  double* b1 = dyn_smem();
+  double* b2 = b1 + b2_offset<D, d>();
   const double sig = sqrt(innov_tot[0] / count);
-  copy(D * D, lastc ? pterm : ps + (c + 1) * S::DD, Pn);
+  stage(D, D, lastc ? pterm : ps + (c + 1) * S::DD, D, Pn, D);
   auto emit = [&](int64_t n, const double* Pnode) {
     if (threadIdx.x == 0) G::taus(a.grid, n, tt, tti);
-    copy(D * D, Pnode, Ac);
-    psd_factor(D, Ac, D, F, D, perm, s.red);
-    for (int idx = threadIdx.x; idx < D * D; idx += kBT) {
-      const int r = idx / D;
-      if (o.cov) o.cov[n * S::DD + idx] = tt[r % B] * F[idx] * sig;
+    stage(D, D, Pnode, D, b1, ls);
+    psd_factor_smem(D, b1, ls, b2, ls, perm, s.red);
+    if (o.cov) {
+      double* oc = o.cov + n * S::DD;
+      for (int base = threadIdx.x; base < D * D; base += 4 * kBT) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int idx = base + u * kBT;
+          if (idx < D * D) {
+            const int r = idx / D;
+            oc[idx] = tt[r % B] * b2[r * ls + idx % D] * sig;
+          }
+        }
+      }
     }
     for (int r = threadIdx.x; r < D; r += kBT) {
       if (o.means) o.means[n * D + r] = eta_out[n * D + r];
@@ -921,13 +992,16 @@ __global__ void __launch_bounds__(kBT) k_big_fin_bwd(BigArgs a, const double* E_
   for (int64_t k = e - 1; k >= s0; --k) {
     G::step_consts(s, a.grid, k);
     const double* Ek = E_in + k * S::DD;
-    smooth_cov<D, d>(s, Ek, pf + k * S::DD, a.qq, M1, T1, T2);
-    gemm<false, false>(D, D, D, 1.0, Ek, D, Pn, D, 0.0, T1, D);   // E P^s_{k+1}
-    copy(D * D, M1, Pk);
-    gemm<false, true>(D, D, D, 1.0, T1, D, Ek, D, 1.0, Pk, D);    // + E P E^T
+    // P^s_k = (I - E phi) P+ (I - E phi)^T + E (Q Q^T + P^s_{k+1}) E^T
+    smooth_joseph<D, d>(s, Ek, pf + k * S::DD, T1, T2, Pk);
+    axpby_eye(D, 1.0, a.qq, 1.0, Pn, 0.0, T3);
+    gemm<false, false>(D, D, D, 1.0, Ek, D, T3, D, 0.0, T2, D);   // E (Q Q^T + P^s_{k+1})
+    gemm<false, true>(D, D, D, 1.0, T2, D, Ek, D, 1.0, Pk, D);    // .. E^T
     symmetrize(D, Pk, D);
     emit(k, Pk);
-    copy(D * D, Pk, Pn);
+    double* t = Pn;
+    Pn = Pk;
+    Pk = t;
   }
 }
 

@@ -4,8 +4,10 @@
 // that live in its global-memory workspace (L2-resident) and its shared
 // memory.  Products run on the FP64 tensor pipe (DMMA, mma.sync m8n8k4
 // .f64): at this size they are real dense contractions (SURVEY.md §8(d):
-// AI ~ 200 flop/B).  Factorisations (Cholesky, LU) are column-serial with
-// CTA-wide trailing updates.
+// AI ~ 200 flop/B).  Cholesky and the triangular solves are blocked (8-wide
+// panels, DMMA trailing updates) on matrices resident in shared memory at a
+// bank-conflict-free stride (smem_ld); global operands arrive by cp.async.
+// The chain kernels' LU (partial pivoting) is column-serial.
 //
 // Every routine is called by all threads of the CTA and ends with a
 // __syncthreads(); matrices are row-major with an explicit leading dimension.
@@ -24,7 +26,7 @@ constexpr int kBW = kBT / 32;
 // The kernels' dynamic shared memory: the staging area of every routine
 // below (they do not nest).  Size: big_smem_bytes<D>() (big.cuh).
 __device__ __forceinline__ double* dyn_smem() {
-  extern __shared__ double big_dyn_smem[];
+  extern __shared__ __align__(16) double big_dyn_smem[];
   return big_dyn_smem;
 }
 
@@ -32,6 +34,74 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b,
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};"
                : "=d"(d0), "=d"(d1)
                : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
+// Asynchronous global -> shared copies (cp.async, 16 bytes each): all of a
+// matrix in flight at once, no registers, then one wait + barrier.
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// dst (rows x cols, stride ldd) <- src (stride lds).  Global -> shared with
+// even strides and 16-byte aligned bases: cp.async; otherwise 8 loads in
+// flight per thread (generic pointers: without batching every load waits
+// on the previous store).
+__device__ __forceinline__ void stage(int rows, int cols, const double* src, int lds, double* dst, int ldd) {
+  const bool async = __isGlobal(src) && __isShared(dst) && !(cols & 1) && !(lds & 1) && !(ldd & 1) &&
+                     !(reinterpret_cast<uintptr_t>(src) & 15) && !(reinterpret_cast<uintptr_t>(dst) & 15);
+  if (async) {
+    const int h = cols >> 1;
+    for (int idx = threadIdx.x; idx < rows * h; idx += kBT) {
+      const int r = idx / h, q = idx - r * h;
+      cp_async16(dst + r * ldd + 2 * q, src + r * lds + 2 * q);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    return;
+  }
+  const int n = rows * cols;
+  for (int base = threadIdx.x; base < n; base += 8 * kBT) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * kBT;
+      v[u] = idx < n ? src[(idx / cols) * lds + idx % cols] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * kBT;
+      if (idx < n) dst[(idx / cols) * ldd + idx % cols] = v[u];
+    }
+  }
+  __syncthreads();
+}
+
+// Z = alpha X + beta Y + gamma I (n x n, stride n; Z may alias X or Y),
+// 8 elements in flight per thread.
+__device__ __forceinline__ void axpby_eye(int n, double alpha, const double* X, double beta, const double* Y,
+                                          double gamma, double* Z) {
+  const int nn = n * n;
+  for (int base = threadIdx.x; base < nn; base += 8 * kBT) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * kBT;
+      v[u] = 0.0;
+      if (idx < nn) {
+        v[u] = alpha * X[idx];
+        if (Y) v[u] = fma(beta, Y[idx], v[u]);
+        if (idx / n == idx % n) v[u] += gamma;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * kBT;
+      if (idx < nn) Z[idx] = v[u];
+    }
+  }
+  __syncthreads();
 }
 
 // C[M x N] = alpha op(A)[M x K] op(B)[K x N] + beta C (beta = 0: C is not
@@ -57,36 +127,24 @@ __device__ void gemm(int M, int N, int K, double alpha, const double* A, int lda
                      double beta, double* C, int ldc) {
   double* sm = dyn_smem();
   const int ldb_s = smem_ld(N);
-  for (int base = threadIdx.x; base < K * N; base += 4 * kBT) {
-    double v[4];
+  if (!TB) {
+    stage(K, N, B, ldb, sm, ldb_s);
+  } else {  // B stored N x K: read along k, 8 loads in flight
+    for (int base = threadIdx.x; base < K * N; base += 8 * kBT) {
+      double v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {  // 4 loads in flight per thread
-      const int idx = base + u * kBT;
-      if (idx < K * N) {
-        if (TB) {  // B stored N x K: read along k
-          const int n = idx / K, k = idx - n * K;
-          v[u] = B[n * ldb + k];
-        } else {
-          const int k = idx / N, n = idx - k * N;
-          v[u] = B[k * ldb + n];
-        }
+      for (int u = 0; u < 8; ++u) {
+        const int idx = base + u * kBT;
+        v[u] = idx < K * N ? B[(idx / K) * ldb + idx % K] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = base + u * kBT;
+        if (idx < K * N) sm[(idx % K) * ldb_s + idx / K] = v[u];
       }
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int idx = base + u * kBT;
-      if (idx < K * N) {
-        if (TB) {
-          const int n = idx / K, k = idx - n * K;
-          sm[k * ldb_s + n] = v[u];
-        } else {
-          const int k = idx / N, n = idx - k * N;
-          sm[k * ldb_s + n] = v[u];
-        }
-      }
-    }
+    __syncthreads();
   }
-  __syncthreads();
   gemm_core<TA>(M, N, K, alpha, A, lda, sm, ldb_s, beta, C, ldc);
 }
 
@@ -196,27 +254,6 @@ __device__ __forceinline__ void copy(int n, const double* src, double* dst) {
   __syncthreads();
 }
 
-// dst (rows x cols, stride ldd) <- src (stride lds), 8 loads in flight per
-// thread (generic pointers: without batching every load waits on the
-// previous store).
-__device__ __forceinline__ void stage(int rows, int cols, const double* src, int lds, double* dst, int ldd) {
-  const int n = rows * cols;
-  for (int base = threadIdx.x; base < n; base += 8 * kBT) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int idx = base + u * kBT;
-      v[u] = idx < n ? src[(idx / cols) * lds + idx % cols] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int idx = base + u * kBT;
-      if (idx < n) dst[(idx / cols) * ldd + idx % cols] = v[u];
-    }
-  }
-  __syncthreads();
-}
-
 // (A + A^T) / 2 in place (n x n).
 __device__ __forceinline__ void symmetrize(int n, double* A, int lda) {
   for (int i = threadIdx.x >> 5; i < n; i += kBW)
@@ -250,81 +287,6 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   for (int w = 0; w < kBW; ++w) m += red[w];
   __syncthreads();
   return m;
-}
-
-// In-place lower Cholesky factor of the SPD n x n matrix A (upper triangle
-// zeroed), factored in shared memory (dyn_smem: >= n (n + 1) doubles).
-// Right-looking, one column per step.  Returns true (CTA-uniform) when a
-// pivot is not positive or |L_jj| <= 1e-13 max_i |L_ii| — the reference's
-// singular-factor test on the factor (linalg.cpp:54-62).
-__device__ bool potrf(int n, double* A, int lda, double* red) {
-  double* sm = dyn_smem();
-  __shared__ double s_d[kBT];
-  const int ls = n + 1;
-  for (int idx = threadIdx.x; idx < n * n; idx += kBT) sm[(idx / n) * ls + idx % n] = A[(idx / n) * lda + idx % n];
-  __syncthreads();
-  // right-looking on unscaled columns: A(j+1) = A(j) - a_j a_j^T / d_j, one
-  // barrier per column; L[i][j] = a_ij / sqrt(d_j) at the end
-  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
-  bool bad = false;
-  for (int j = 0; j < n; ++j) {
-    const double dj = sm[j * ls + j];
-    bad |= !(dj > 0.0);
-    const double inv = dj > 0.0 ? 1.0 / dj : 0.0;
-    if (threadIdx.x == 0) s_d[j] = dj;
-    for (int i = j + 1 + ty; i < n; i += 16) {
-      const double lij = sm[i * ls + j] * inv;
-      for (int k = j + 1 + tx; k <= i; k += 16) sm[i * ls + k] = fma(-lij, sm[k * ls + j], sm[i * ls + k]);
-    }
-    __syncthreads();
-  }
-  double dmax = 0.0;
-  for (int idx = threadIdx.x; idx < n * n; idx += kBT) {
-    const int i = idx / n, k = idx - (idx / n) * n;
-    const double dk = s_d[k];
-    const double v = (k > i || !(dk > 0.0)) ? 0.0 : sm[i * ls + k] / sqrt(dk);
-    A[i * lda + k] = v;
-    if (k == i) dmax = fmax(dmax, fabs(v));
-  }
-  __syncthreads();
-  const double mx = block_max(dmax, red);
-  double mine = bad ? 1.0 : 0.0;
-  for (int i = threadIdx.x; i < n; i += kBT) mine = fmax(mine, fabs(A[i * lda + i]) <= 1e-13 * mx ? 1.0 : 0.0);
-  return block_max(mine, red) > 0.0;
-}
-
-// W = L^-1 for the lower-triangular n x n L (W may alias L), inverted in
-// place in shared memory (dyn_smem: >= n (n + 1) doubles) column by column from
-// the right: W[i][j] = -W[j][j] sum_{k=j+1..i} W[i][k] L[k][j].
-__device__ void trtri_lower(int n, const double* L, int ldl, double* W, int ldw) {
-  double* sl = dyn_smem();
-  const int ls = n + 1;
-  double* sw = sl + n * ls;
-  for (int idx = threadIdx.x; idx < n * n; idx += kBT) {
-    const int i = idx / n, k = idx - (idx / n) * n;
-    sl[i * ls + k] = (k > i) ? 0.0 : L[i * ldl + k];
-    sw[i * ls + k] = 0.0;
-  }
-  __syncthreads();
-  // W column j from the right: W[i][j] = -W[j][j] sum_{k=j+1..i} W[i][k] L[k][j]
-  // (reads W columns > j, L column j: one barrier per column); rows split
-  // over the threads, each row's dot split over 4 lanes
-  const int q4 = threadIdx.x & 3, rgrp = threadIdx.x >> 2;
-  for (int j = n - 1; j >= 0; --j) {
-    const double inv = 1.0 / sl[j * ls + j];
-    for (int base = j; base < n; base += kBT / 4) {  // warp-uniform trip count (shuffles below)
-      const int i = base + rgrp;
-      double acc = 0.0;
-      if (i > j && i < n)
-        for (int k = j + 1 + q4; k <= i; k += 4) acc = fma(sw[i * ls + k], sl[k * ls + j], acc);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      if (q4 == 0 && i < n) sw[i * ls + j] = (i == j) ? inv : -inv * acc;
-    }
-    __syncthreads();
-  }
-  for (int idx = threadIdx.x; idx < n * n; idx += kBT) W[(idx / n) * ldw + idx % n] = sw[(idx / n) * ls + idx % n];
-  __syncthreads();
 }
 
 // LU with partial pivoting of the n x n A, then X <- A^-1 X for the n x m
@@ -404,7 +366,7 @@ __device__ void lu_solve(int n, double* A, int lda, int m, double* X, int ldx) {
 
 
 // ------------------------------------------------ blocked, smem-resident ---
-// The column-serial factorisations above pay one CTA barrier and one pass of
+// A column-serial factorisation pays one CTA barrier and one pass of
 // shared-memory latency per column.  The blocked forms below work on
 // matrices already staged in shared memory (stride ls), 8 columns per panel:
 // the panel is factored column by column on its 8 columns only, the trailing
@@ -586,6 +548,52 @@ __device__ void trsm_right_lower_n(int m, int n, const double* sl, int ll, doubl
             if (c2 < w) acc = fma(-x[c2], sl[(jb + c2) * ll + jb + c], acc);
           x[c] = acc * s_rd[jb + c];
           sy[r * ly + jb + c] = x[c];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// L X = B in place (B: n x m in shared memory, stride lx; L: n x n lower,
+// stride ll): row blocks of 8 top to bottom, the update by the solved rows on
+// DMMA (warps over 8-column tiles), the 8-row forward substitution one
+// column per thread.
+__device__ void trsm_left_lower(int n, int m, const double* sl, int ll, double* sx, int lx) {
+  __shared__ double s_rd[128];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gr = lane >> 2, tg = lane & 3;
+  for (int j = threadIdx.x; j < n; j += kBT) s_rd[j] = 1.0 / sl[j * ll + j];
+  __syncthreads();
+  for (int ib = 0; ib < n; ib += 8) {
+    const int w = min(8, n - ib);
+    if (ib > 0) {  // X[ib:ib+w, :] -= L[ib:ib+w, 0:ib] X[0:ib, :]
+      for (int ct = warp; ct * 8 < m; ct += kBW) {
+        const int r = ib + gr, cc = ct * 8 + 2 * tg;
+        const bool rin = gr < w;
+        double c0 = (rin && cc < m) ? sx[r * lx + cc] : 0.0;
+        double c1 = (rin && cc + 1 < m) ? sx[r * lx + cc + 1] : 0.0;
+        const int bc = ct * 8 + gr;  // B[k][col] = X[k][ct 8 + col]
+        for (int k0 = 0; k0 < ib; k0 += 4) {
+          const double a = rin ? -sl[r * ll + k0 + tg] : 0.0;
+          const double b = bc < m ? sx[(k0 + tg) * lx + bc] : 0.0;
+          dmma(c0, c1, a, b, c0, c1);
+        }
+        if (rin && cc < m) sx[r * lx + cc] = c0;
+        if (rin && cc + 1 < m) sx[r * lx + cc + 1] = c1;
+      }
+      __syncthreads();
+    }
+    for (int j = threadIdx.x; j < m; j += kBT) {
+      double x[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c < w) {
+          double acc = sx[(ib + c) * lx + j];
+#pragma unroll
+          for (int c2 = 0; c2 < c; ++c2) acc = fma(-sl[(ib + c) * ll + ib + c2], x[c2], acc);
+          x[c] = acc * s_rd[ib + c];
+          sx[(ib + c) * lx + j] = x[c];
         }
       }
     }
