@@ -863,27 +863,36 @@ __global__ void __launch_bounds__(kBT) k_big_chain_fin(int64_t nc, const double*
   }
 }
 
-// Pivoted Cholesky of the PSD n x n A (destroyed): F (n x n) with F F^T = A,
-// F = Pi L; pivots below 1e-15 max diag end the factorisation (remaining
-// columns zero).  A (stride la) and F (stride lf) in shared memory: the remaining diagonal is tracked in s_dg, the pivot
-// order in perm; only the lower triangle (in pivot order) is updated.
-__device__ void psd_factor_smem(int n, double* A, int la, double* F, int lf, int* perm, double* red) {
+// Pivoted Cholesky of the symmetric PSD n x n A (shared memory, stride la,
+// both triangles; destroyed): A = Pi L L^T Pi^T with the largest remaining
+// diagonal as pivot; a pivot <= 1e-15 max diag ends the factorisation
+// (remaining columns zero).  Blocked: 8-column panels, each column one
+// symmetric row/column swap and one left-looking column update inside the
+// panel (2 barriers), the trailing update a DMMA rank-8 product on full
+// tiles (the trailing block stays exactly symmetric for the swaps).  On
+// return L is in A's lower triangle (pivot order), perm[i] = original index
+// of pivot row i; returns the rank.
+__device__ int psd_factor_smem(int n, double* A, int la, int* perm, double* red) {
   __shared__ double s_dg[128];
-  __shared__ double s_d;
-  for (int idx = threadIdx.x; idx < n * n; idx += kBT) F[(idx / n) * lf + idx % n] = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gr = lane >> 2, tg = lane & 3;
   double mloc = 0.0;
   for (int i = threadIdx.x; i < n; i += kBT) {
     perm[i] = i;
     s_dg[i] = A[i * la + i];
     mloc = fmax(mloc, A[i * la + i]);
   }
-  const double dmax0 = block_max(mloc, red);  // (syncs)
-  for (int j = 0; j < n; ++j) {
-    if (threadIdx.x < 32) {  // pivot: largest remaining diagonal
+  const double tol = 1e-15 * block_max(mloc, red);  // (syncs)
+  int rank = n;
+  for (int j0 = 0; j0 < n && rank == n; j0 += 8) {
+    const int w = min(8, n - j0);
+    for (int c = 0; c < w; ++c) {
+      const int j = j0 + c;
+      // pivot: every warp finds it (no broadcast barrier)
       double best = -1.0;
       int bi = j;
-      for (int i = j + threadIdx.x; i < n; i += 32) {
-        const double v = s_dg[perm[i]];
+      for (int i = j + lane; i < n; i += 32) {
+        const double v = s_dg[i];
         if (v > best) {
           best = v;
           bi = i;
@@ -898,38 +907,73 @@ __device__ void psd_factor_smem(int n, double* A, int la, double* F, int lf, int
           bi = oi;
         }
       }
-      if (threadIdx.x == 0) {
-        s_d = best;
-        const int t = perm[j];
-        perm[j] = perm[bi];
-        perm[bi] = t;
+      if (!(best > tol)) {  // CTA-uniform: rank j
+        rank = j;
+        break;
       }
-    }
-    __syncthreads();
-    if (!(s_d > 1e-15 * dmax0)) break;  // CTA-uniform
-    const int pj = perm[j];
-    const double l = sqrt(s_d), inv = 1.0 / l;
-    for (int i = j + threadIdx.x; i < n; i += kBT) {
-      const int pi = perm[i];
-      const double v = (i == j) ? l : A[pi * la + pj] * inv;
-      F[pi * lf + j] = v;
-      if (i > j) s_dg[pi] -= v * v;
-    }
-    __syncthreads();
-    // Schur complement, lower triangle in pivot order (ii >= kk)
-    for (int ii = j + 1 + (threadIdx.x >> 5); ii < n; ii += kBW) {
-      const int pi = perm[ii];
-      const double fi = F[pi * lf + j];
-      for (int kk = j + 1 + (threadIdx.x & 31); kk <= ii; kk += 32) {
-        const int pk = perm[kk];
-        const double v = fma(-fi, F[pk * lf + j], A[pi * la + pk]);
-        A[pi * la + pk] = v;
-        A[pk * la + pi] = v;
+      const int p = bi;
+      if (p != j) {  // rows j <-> p (all columns), then (below) columns per row
+        for (int t = threadIdx.x; t < n; t += kBT) {
+          const double x = A[j * la + t];
+          A[j * la + t] = A[p * la + t];
+          A[p * la + t] = x;
+        }
+        if (threadIdx.x == 0) {
+          const double x = s_dg[j];
+          s_dg[j] = s_dg[p];
+          s_dg[p] = x;
+          const int q = perm[j];
+          perm[j] = perm[p];
+          perm[p] = q;
+        }
       }
+      __syncthreads();
+      // thread per row i >= j: swap its columns j <-> p, then
+      // L_ij = (A_ij - sum_{c' in panel, < j} L_ic' L_jc') / L_jj
+      const double l = sqrt(s_dg[j]), inv = 1.0 / l;
+      for (int i = j + threadIdx.x; i < n; i += kBT) {
+        double v = A[i * la + p];
+        if (p != j) {
+          A[i * la + p] = A[i * la + j];
+        }
+        if (i == j) {
+          A[i * la + j] = l;
+        } else {
+          for (int c2 = j0; c2 < j; ++c2) v = fma(-A[i * la + c2], A[j * la + c2], v);
+          v *= inv;
+          A[i * la + j] = v;
+          s_dg[i] -= v * v;
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
+    if (rank < n) break;
+    // trailing update A22 -= L21 L21^T (full tiles), rank w, on DMMA
+    const int r0b = j0 + w, M = n - r0b;
+    if (M > 0) {
+      const int tiles = (M + 7) / 8;
+      for (int q = warp; q < tiles * tiles; q += kBW) {
+        const int ti = q / tiles, tj = q - ti * tiles;
+        const int rr = r0b + ti * 8 + gr, cc = r0b + tj * 8 + 2 * tg, rb = r0b + tj * 8 + gr;
+        double c0 = (rr < n && cc < n) ? A[rr * la + cc] : 0.0;
+        double c1 = (rr < n && cc + 1 < n) ? A[rr * la + cc + 1] : 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 4) {
+          if (kk < w) {
+            const int k = j0 + kk + tg;
+            const double a = (rr < n && kk + tg < w) ? -A[rr * la + k] : 0.0;
+            const double b = (rb < n && kk + tg < w) ? A[rb * la + k] : 0.0;
+            dmma(c0, c1, a, b, c0, c1);
+          }
+        }
+        if (rr < n && cc < n) A[rr * la + cc] = c0;
+        if (rr < n && cc + 1 < n) A[rr * la + cc + 1] = c1;
+      }
+      __syncthreads();
+    }
   }
   __syncthreads();
+  return rank;
 }
 
 struct BigOut {
@@ -958,22 +1002,21 @@ __global__ void __launch_bounds__(kBT) k_big_fin_bwd(BigArgs a, const double* E_
   double *Pn = w, *T1 = w + 2 * S::DD, *T2 = w + 3 * S::DD, *Pk = w + 4 * S::DD, *T3 = w + 5 * S::DD;
   constexpr int ls = smem_ld(D);
   double* b1 = dyn_smem();
-  double* b2 = b1 + b2_offset<D, d>();
   const double sig = sqrt(innov_tot[0] / count);
   stage(D, D, lastc ? pterm : ps + (c + 1) * S::DD, D, Pn, D);
   auto emit = [&](int64_t n, const double* Pnode) {
     if (threadIdx.x == 0) G::taus(a.grid, n, tt, tti);
-    stage(D, D, Pnode, D, b1, ls);
-    psd_factor_smem(D, b1, ls, b2, ls, perm, s.red);
-    if (o.cov) {
+    if (o.cov) {  // F = Pi L, row perm[i] of F = row i of L, scaled by T_n sigma
+      stage(D, D, Pnode, D, b1, ls);
+      const int rank = psd_factor_smem(D, b1, ls, perm, s.red);
       double* oc = o.cov + n * S::DD;
       for (int base = threadIdx.x; base < D * D; base += 4 * kBT) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int idx = base + u * kBT;
           if (idx < D * D) {
-            const int r = idx / D;
-            oc[idx] = tt[r % B] * b2[r * ls + idx % D] * sig;
+            const int i = idx / D, cc = idx - i * D, pi = perm[i];
+            oc[pi * D + cc] = (cc <= i && cc < rank) ? tt[pi % B] * b1[i * ls + cc] * sig : 0.0;
           }
         }
       }
