@@ -388,7 +388,7 @@ struct Big {
 // Dynamic shared memory of the kernels: b1 (offset 0: the staging area of
 // the big_la.cuh routines and of cov_update_parts) and b2 (a resident D x D
 // matrix, stride smem_ld(D)) after it; the chain kernels' LU needs
-// D (D + 1) + D (D + 2).
+// D smem_ld(2 D + 1).
 template <int D, int d = 28>
 constexpr int b2_offset() {
   constexpr int ls = smem_ld(D), scratch = d * smem_ld(D) + 2 * d * smem_ld(d);
@@ -396,7 +396,7 @@ constexpr int b2_offset() {
 }
 template <int D>
 constexpr size_t big_smem_bytes(bool) {
-  constexpr size_t two = size_t(b2_offset<D>()) + size_t(D) * smem_ld(D), lu = size_t(D) * (2 * D + 3);
+  constexpr size_t two = size_t(b2_offset<D>()) + size_t(D) * smem_ld(D), lu = size_t(D) * smem_ld(2 * D + 1);
   return sizeof(double) * (two > lu ? two : lu);
 }
 
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kBT) k_big_chain_fwd(BigArgs a, const double* 
                                                        int first, const double* carry) {
   using S = Slots<D, d>;
   double *M = scratch, *X = scratch + S::DD, *T = X + int64_t(D) * (D + 1);
-  double *m = T + S::DD, *Pc = m + D;
+  double* m = T + S::DD;
   const int64_t stride = 3 * S::DD + 2 * D;
   // chunk 0: its aggregate absorbed the initial distribution (A = 0), or (a
   // shard) starts from the carry
@@ -527,26 +527,22 @@ __global__ void __launch_bounds__(kBT) k_big_chain_fwd(BigArgs a, const double* 
       continue;
     }
     const double* pm = (c == 0) ? carry : prefix + (c - 1) * (S::DD + D);
-    copy(D, pm, m);
-    copy(D * D, pm + D, Pc);
+    const double* Pcg = pm + D;
     // M = I + Pc Lambda; X = [Pc | m + Pc eta]
-    gemm<false, false>(D, D, D, 1.0, Pc, D, Lam, D, 0.0, M, D);
-    for (int i = threadIdx.x; i < D; i += kBT) M[i * D + i] += 1.0;
-    for (int idx = threadIdx.x; idx < D * D; idx += kBT) X[(idx / D) * (D + 1) + idx % D] = Pc[idx];
-    __syncthreads();
-    for (int i = threadIdx.x; i < D; i += kBT) {
-      double acc = m[i];
-      for (int k = 0; k < D; ++k) acc = fma(Pc[i * D + k], ec[k], acc);
-      X[i * (D + 1) + D] = acc;
+    gemm<false, false>(D, D, D, 1.0, Pcg, D, Lam, D, 0.0, M, D);
+    gemv<false>(D, D, 1.0, Pcg, D, ec, 0.0, m);
+    for (int idx = threadIdx.x; idx < D * (D + 1); idx += kBT) {
+      const int r = idx / (D + 1), j = idx - r * (D + 1);
+      X[idx] = j < D ? Pcg[r * D + j] : m[r] + pm[r];
+      if (j == r) M[r * D + r] += 1.0;
     }
     __syncthreads();
     lu_solve(D, M, D, D + 1, X, D + 1);  // X = [P_s | m_s]
     // out.m = A m_s + b; out.P = A P_s A^T + Pa
-    for (int i = threadIdx.x; i < D; i += kBT) {
-      double acc = bc[i];
-      for (int k = 0; k < D; ++k) acc = fma(Ac[i * D + k], X[k * (D + 1) + D], acc);
-      out[i] = acc;
-    }
+    for (int r = threadIdx.x; r < D; r += kBT) m[r] = X[r * (D + 1) + D];
+    __syncthreads();
+    copy(D, bc, out);
+    gemv<false>(D, D, 1.0, Ac, D, m, 1.0, out);
     gemm<false, false>(D, D, D, 1.0, Ac, D, X, D + 1, 0.0, T, D);          // A P_s
     copy(D * D, Pa, out + D);
     gemm<false, true>(D, D, D, 1.0, T, D, Ac, D, 1.0, out + D, D);         // + A P_s A^T

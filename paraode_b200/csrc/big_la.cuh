@@ -290,24 +290,29 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 }
 
 // LU with partial pivoting of the n x n A, then X <- A^-1 X for the n x m
-// right-hand sides (in place); A and X are staged in shared memory (dyn_smem:
-// >= n (n + 1) + n (m + 1) doubles).  A is destroyed.
-__device__ void lu_solve(int n, double* A, int lda, int m, double* X, int ldx) {
-  double* sm = dyn_smem();
-  __shared__ int s_p;
-  __shared__ double s_inv;
-  const int la = n + 1, lx = m + 1;
-  double* sa = sm;
-  double* sx = sm + n * la;
-  for (int idx = threadIdx.x; idx < n * n; idx += kBT) sa[(idx / n) * la + idx % n] = A[(idx / n) * lda + idx % n];
-  for (int idx = threadIdx.x; idx < n * m; idx += kBT) sx[(idx / m) * lx + idx % m] = X[(idx / m) * ldx + idx % m];
-  __syncthreads();
-  for (int j = 0; j < n; ++j) {
-    if (threadIdx.x < 32) {  // pivot: argmax |A[i][j]|, i >= j
+// right-hand sides (in place).  [A | X] is staged in shared memory as one
+// augmented n x (n + m) matrix (dyn_smem: n smem_ld(n + m) doubles), so the
+// eliminations carry the right-hand sides along.  Blocked: 8-column panels
+// (per column: pivot found by every warp, one row swap, one rank-1 update
+// of the panel: 2 barriers), the panel's rows of U by an 8-row unit-lower
+// solve, the trailing update (right-hand sides included) a DMMA rank-8
+// product; then a blocked back substitution on DMMA.  A is not modified.
+__device__ void lu_solve(int n, const double* A, int lda, int m, double* X, int ldx) {
+  __shared__ double s_rd[128];
+  double* g = dyn_smem();
+  const int nm = n + m, lg = smem_ld(nm);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gr = lane >> 2, tg = lane & 3;
+  stage(n, n, A, lda, g, lg);
+  stage(n, m, X, ldx, g + n, lg);
+  for (int j0 = 0; j0 < n; j0 += 8) {
+    const int w = min(8, n - j0);
+    for (int c = 0; c < w; ++c) {
+      const int j = j0 + c;
       double best = -1.0;
       int bi = j;
-      for (int i = j + threadIdx.x; i < n; i += 32) {
-        const double v = fabs(sa[i * la + j]);
+      for (int i = j + lane; i < n; i += 32) {
+        const double v = fabs(g[i * lg + j]);
         if (v > best) {
           best = v;
           bi = i;
@@ -322,48 +327,109 @@ __device__ void lu_solve(int n, double* A, int lda, int m, double* X, int ldx) {
           bi = oi;
         }
       }
-      if (threadIdx.x == 0) {
-        s_p = bi;
-        s_inv = 1.0 / sa[bi * la + j];
+      if (bi != j) {
+        for (int t = threadIdx.x; t < nm; t += kBT) {
+          const double x = g[j * lg + t];
+          g[j * lg + t] = g[bi * lg + t];
+          g[bi * lg + t] = x;
+        }
       }
-    }
-    __syncthreads();
-    const int p = s_p;
-    if (p != j) {
-      for (int k = threadIdx.x; k < n + m; k += kBT) {
-        double* rj = k < n ? sa + j * la + k : sx + j * lx + (k - n);
-        double* rp = k < n ? sa + p * la + k : sx + p * lx + (k - n);
-        const double t = *rj;
-        *rj = *rp;
-        *rp = t;
+      __syncthreads();
+      const double inv = 1.0 / g[j * lg + j];
+      for (int i = j + 1 + threadIdx.x; i < n; i += kBT) {
+        const double l = g[i * lg + j] * inv;
+        g[i * lg + j] = l;
+        for (int k = j + 1; k < j0 + w; ++k) g[i * lg + k] = fma(-l, g[j * lg + k], g[i * lg + k]);
       }
       __syncthreads();
     }
-    const double inv = s_inv;
-    const int ncol = n - j - 1;
-    const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
-    for (int i = j + 1 + ty; i < n; i += kBT / 16) {
-      const double l = sa[i * la + j] * inv;
-      for (int c = tx; c < ncol; c += 16) sa[i * la + j + 1 + c] = fma(-l, sa[j * la + j + 1 + c], sa[i * la + j + 1 + c]);
-      for (int c = tx; c < m; c += 16) sx[i * lx + c] = fma(-l, sx[j * lx + c], sx[i * lx + c]);
+    const int t0 = j0 + w;
+    if (t0 < nm) {
+      // U12 = L11^-1 A12 on the panel rows, one column per thread
+      for (int t = t0 + threadIdx.x; t < nm; t += kBT) {
+        double u[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          if (r < w) {
+            double acc = g[(j0 + r) * lg + t];
+#pragma unroll
+            for (int r2 = 0; r2 < r; ++r2) acc = fma(-g[(j0 + r) * lg + j0 + r2], u[r2], acc);
+            u[r] = acc;
+            g[(j0 + r) * lg + t] = acc;
+          }
+        }
+      }
+      __syncthreads();
+      // A22 -= L21 U12 (rows >= t0, columns >= t0 incl. right-hand sides)
+      if (t0 < n) {
+        const int rt = (n - t0 + 7) / 8, ct = (nm - t0 + 7) / 8;
+        for (int q = warp; q < rt * ct; q += kBW) {
+          const int ti = q / ct, tj = q - ti * ct;
+          const int rr = t0 + ti * 8 + gr, cc = t0 + tj * 8 + 2 * tg, bc = t0 + tj * 8 + gr;
+          double c0 = (rr < n && cc < nm) ? g[rr * lg + cc] : 0.0;
+          double c1 = (rr < n && cc + 1 < nm) ? g[rr * lg + cc + 1] : 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 8; kk += 4) {
+            if (kk < w) {
+              const int k = j0 + kk + tg;
+              const double a = (rr < n && kk + tg < w) ? -g[rr * lg + k] : 0.0;
+              const double b = (bc < nm && kk + tg < w) ? g[k * lg + bc] : 0.0;
+              dmma(c0, c1, a, b, c0, c1);
+            }
+          }
+          if (rr < n && cc < nm) g[rr * lg + cc] = c0;
+          if (rr < n && cc + 1 < nm) g[rr * lg + cc + 1] = c1;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  // back substitution U Xs = Y (Y = columns n.. of g), row blocks bottom-up
+  for (int j = threadIdx.x; j < n; j += kBT) s_rd[j] = 1.0 / g[j * lg + j];
+  __syncthreads();
+  double* y = g + n;
+  const int nblk = (n + 7) / 8;
+  for (int bb = nblk - 1; bb >= 0; --bb) {
+    const int ib = bb * 8, w = min(8, n - ib), k0s = ib + w;
+    if (k0s < n) {  // Y[ib:ib+w, :] -= U[ib:ib+w, k0s:n] X[k0s:n, :]
+      for (int ct = warp; ct * 8 < m; ct += kBW) {
+        const int r = ib + gr, cc = ct * 8 + 2 * tg, bc = ct * 8 + gr;
+        const bool rin = gr < w;
+        double c0 = (rin && cc < m) ? y[r * lg + cc] : 0.0;
+        double c1 = (rin && cc + 1 < m) ? y[r * lg + cc + 1] : 0.0;
+        double e0 = 0.0, e1 = 0.0;
+        for (int k0 = k0s; k0 < n; k0 += 8) {
+          const int k = k0 + tg, k2 = k0 + 4 + tg;
+          const double a = (rin && k < n) ? -g[r * lg + k] : 0.0;
+          const double b = (k < n && bc < m) ? y[k * lg + bc] : 0.0;
+          const double a2 = (rin && k2 < n) ? -g[r * lg + k2] : 0.0;
+          const double b2 = (k2 < n && bc < m) ? y[k2 * lg + bc] : 0.0;
+          dmma(c0, c1, a, b, c0, c1);
+          dmma(e0, e1, a2, b2, e0, e1);
+        }
+        if (rin && cc < m) y[r * lg + cc] = c0 + e0;
+        if (rin && cc + 1 < m) y[r * lg + cc + 1] = c1 + e1;
+      }
+      __syncthreads();
+    }
+    for (int t = threadIdx.x; t < m; t += kBT) {
+      double x[8];
+#pragma unroll
+      for (int r = 7; r >= 0; --r) {
+        if (r < w) {
+          double acc = y[(ib + r) * lg + t];
+#pragma unroll
+          for (int r2 = 7; r2 > r; --r2)
+            if (r2 < w) acc = fma(-g[(ib + r) * lg + ib + r2], x[r2], acc);
+          x[r] = acc * s_rd[ib + r];
+          y[(ib + r) * lg + t] = x[r];
+        }
+      }
     }
     __syncthreads();
-    for (int i = j + 1 + threadIdx.x; i < n; i += kBT) sa[i * la + j] *= inv;
-    __syncthreads();
   }
-  // back substitution U x = y, one thread per right-hand side column
-  for (int c = threadIdx.x; c < m; c += kBT) {
-    for (int i = n - 1; i >= 0; --i) {
-      double acc = sx[i * lx + c];
-      for (int k = i + 1; k < n; ++k) acc = fma(-sa[i * la + k], sx[k * lx + c], acc);
-      sx[i * lx + c] = acc / sa[i * la + i];
-    }
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < n * m; idx += kBT) X[(idx / m) * ldx + idx % m] = sx[(idx / m) * lx + idx % m];
-  __syncthreads();
+  stage(n, m, y, lg, X, ldx);
 }
-
 
 // ------------------------------------------------ blocked, smem-resident ---
 // A column-serial factorisation pays one CTA barrier and one pass of
