@@ -37,6 +37,11 @@ def line(problem, nu, lg, fixed_its, reps=2):
         r = P.para_ieks(prob, prior, grid, P.IeksConfig(max_iterations=fixed_its, **NEVER), want_cov=False)
         ts.append(time.perf_counter() - t)
     per_it = min(ts) / fixed_its
+    # marginal cost of an iteration (the finalize, once per solve, cancels):
+    # (T(2 k) - T(k)) / k
+    t = time.perf_counter()
+    P.para_ieks(prob, prior, grid, P.IeksConfig(max_iterations=2 * fixed_its, **NEVER), want_cov=False)
+    marginal = (time.perf_counter() - t - min(ts)) / fixed_its
     if problem != "pleiades":  # warm the default-rule path (graph capture, finalize buffers)
         P.para_ieks(prob, prior, grid, want_cov=True)
     t = time.perf_counter()
@@ -49,7 +54,8 @@ def line(problem, nu, lg, fixed_its, reps=2):
     n = 1 << lg
     return dict(problem=problem, nu=nu, D=prob.dim * (nu + 1), N=n, iterations=c.iterations, converged=c.converged,
                 solve_seconds=wall, time_steps_per_s=n / wall, ms_per_iteration=1e3 * per_it,
-                step_iterations_per_s=n / per_it, fixed_iterations=fixed_its, **oracle(problem, nu, lg),
+                step_iterations_per_s=n / per_it, fixed_iterations=fixed_its,
+                ms_per_iteration_marginal=1e3 * marginal, **oracle(problem, nu, lg),
                 note="wall time through the public API incl. the full SolverReport download")
 
 
