@@ -44,17 +44,19 @@ def test_pleiades_matches_seq_ieks(nu, steps, its, chunk):
     assert np.all(np.isfinite(got.solution_covs))
 
 
-def test_pleiades_2e10_fixture():
-    """N = 2^10 (SURVEY.md §8(d) parity size), 3 equal iterations, against the
-    committed oracle fixture (tools/make_fixtures.py)."""
-    path = os.path.join(GOLDEN, "pleiades_q3_n10_seq_it3.npz")
+@pytest.mark.parametrize("name", ["pleiades_q3_n10_seq_it3", "pleiades_q3_n12_seq_it2"])
+def test_pleiades_fixture(name):
+    """N = 2^10 (3 iterations) and 2^12 (2 iterations), the SURVEY.md §8(d)
+    parity sizes, at equal iteration counts against the committed oracle
+    fixtures (tools/make_fixtures.py)."""
+    path = os.path.join(GOLDEN, name + ".npz")
     if not os.path.exists(path):
         pytest.skip("fixture not generated")
     z = np.load(path)
     meta = json.loads(str(z["meta"]))
     got = gpu_solve(P, meta, max_iterations=meta["iterations"], **NEVER)
     assert np.allclose(got.objective_trace, z["objective_trace"], rtol=1e-8)
-    compare(got, z, meta, "pleiades q3 N=2^10 (fixture)", alternatives(P, meta, meta["iterations"]))
+    compare(got, z, meta, f"pleiades q3 N={meta['steps']} (fixture)", alternatives(P, meta, meta["iterations"]))
 
 
 def test_pleiades_default_rule_outcome_matches_oracle():

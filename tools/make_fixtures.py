@@ -56,6 +56,7 @@ CASES = {
     # configs[4]: Pleiades (d = 28, IWP(3), D = 112) at the parity sizes of SURVEY.md §8(d)
     "pleiades_q3_n10_seq": ("pleiades", 3, 10, 0, 100, False, 64),
     "pleiades_q3_n10_seq_it3": ("pleiades", 3, 10, 0, 3, True, 64),
+    "pleiades_q3_n12_seq_it2": ("pleiades", 3, 12, 0, 2, True, 64),
 }
 
 
