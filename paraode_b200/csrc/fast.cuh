@@ -81,4 +81,25 @@ __device__ __forceinline__ double ipow(double h, int k) {
   return pow(h, double(k));
 }
 
+
+// Node times for a backward loop over steps k = e-1 down to s: step(k)
+// returns h_k = t_k - t_{k-1} (node 0 of the time axis, origin: t_1 - t_0)
+// and issues the load of t_{k-2} one step ahead.  A shard's grid pointer is
+// offset into the global grid, so t_{-1} is its left neighbour's node.
+struct BwdGrid {
+  const double* g;
+  int origin;
+  double tk, tkm;
+  __device__ BwdGrid(const double* grid, int org, int64_t k) : g(grid), origin(org) {
+    tk = grid[k];
+    tkm = (k >= 1 || !org) ? grid[k - 1] : 0.0;
+  }
+  __device__ double step(int64_t k) {
+    const double h = (k == 0 && origin) ? g[1] - g[0] : tk - tkm;
+    tk = tkm;
+    tkm = (k >= 2 || (k == 1 && !origin)) ? g[k - 2] : 0.0;
+    return h;
+  }
+};
+
 }  // namespace pode

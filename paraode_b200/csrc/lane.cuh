@@ -295,18 +295,29 @@ struct Model {
       for (int j = 0; j < D; ++j) cm[r][j] = (j <= r) ? m[r][j] : 0.0;
   }
 
-  // origin: local node 0 is global node 0 (its scale uses the first step).
-  __device__ static void taus(const double* grid, int origin, int64_t n, double (&t)[B], double (&ti)[B]) {
-    const double h = (n == 0 && origin) ? grid[1] - grid[0] : grid[n] - grid[n - 1];
-    const double rh = sqrt(h);
-    double fact = 1.0;
+  // T_n = diag(sqrt(h) h^k / k!), k = q - i, for the incoming step h
+  // (ieks.cpp:28-33), and its inverse from one division:
+  // T^-1 = k! h^-k / sqrt(h) (1 / sqrt(h) = sqrt(h) / h).
+  __device__ static void taus_h(double h, double (&t)[B], double (&ti)[B]) {
+    const double rh = sqrt(h), ih = 1.0 / h, irh = rh * ih;
+    double hp = 1.0, ihp = 1.0, fact = 1.0;
 #pragma unroll
-    for (int i = q; i >= 0; --i) {
-      const int k = q - i;
-      if (k > 0) fact *= k;
-      t[i] = rh * ipow(h, k) / fact;
-      ti[i] = 1.0 / t[i];
+    for (int k = 0; k <= q; ++k) {
+      if (k > 0) {
+        hp *= h;
+        ihp *= ih;
+        fact *= k;
+      }
+      t[q - k] = k <= 2 ? rh * hp / fact : rh * hp * (1.0 / fact);  // (1/1, 1/2 exact)
+      ti[q - k] = irh * ihp * fact;
     }
+  }
+  // origin: local node 0 is global node 0 (its scale uses the first step).
+  __device__ static double step_h(const double* grid, int origin, int64_t n) {
+    return (n == 0 && origin) ? grid[1] - grid[0] : grid[n] - grid[n - 1];
+  }
+  __device__ static void taus(const double* grid, int origin, int64_t n, double (&t)[B], double (&ti)[B]) {
+    taus_h(step_h(grid, origin, n), t, ti);
   }
 };
 
@@ -453,9 +464,14 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks) k_lane_fwd_reduc
   M::taus(a.grid, a.first, s, tk, tki);
   bool bad_sing = false;
   int64_t bad_lin = -1;
+  // node times one step ahead (the grid load's latency overlaps a step)
+  double gcur = a.grid[s], gnext = a.grid[s + 1];
   for (int64_t k = s; k < e; ++k) {
     double tn[B], tni[B], ratio[B], pc[B][B];
-    M::taus(a.grid, a.first, k + 1, tn, tni);
+    const double h = gnext - gcur;
+    gcur = gnext;
+    if (k + 2 <= a.N) gnext = a.grid[k + 2];
+    M::taus_h(h, tn, tni);
 #pragma unroll
     for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
     M::phi_coefs(ratio, pc);
@@ -588,13 +604,18 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
   M::taus(a.grid, a.first, s, tk, tki);
   bool bad_sing = false;
   int64_t bad_lin = -1;
-  // the linearisation point of the next step is loaded one step ahead, so
-  // its global-memory latency overlaps the current step's arithmetic
+  // the linearisation point and the node time of the next step are loaded
+  // one step ahead, so their global-memory latency overlaps the current
+  // step's arithmetic
   double ynext[d];
   gather_y<D, d>(a, lp, c, 1, s + 1, ynext);
+  double gcur = a.grid[s], gnext = a.grid[s + 1];
   for (int64_t k = s; k < e; ++k) {
     double tn[B], tni[B], ratio[B], pc[B][B];
-    M::taus(a.grid, a.first, k + 1, tn, tni);
+    const double h = gnext - gcur;
+    gcur = gnext;
+    if (k + 2 <= a.N) gnext = a.grid[k + 2];
+    M::taus_h(h, tn, tni);
 #pragma unroll
     for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
     M::phi_coefs(ratio, pc);
@@ -845,9 +866,10 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fin_fold(FastArgs a, Fast
   }
   double tn[B], tni[B];
   M::taus(a.grid, a.first, e, tn, tni);
+  BwdGrid bg(a.grid, a.first, e - 1);
   for (int64_t k = e - 1; k >= s; --k) {
     double tk[B], tki[B], ratio[B], pc[B][B];
-    M::taus(a.grid, a.first, k, tk, tki);
+    M::taus_h(bg.step(k), tk, tki);
 #pragma unroll
     for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
     M::phi_coefs(ratio, pc);
@@ -955,9 +977,10 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fin_bwd(FastArgs a, FastC
     for (int r = 0; r < D; ++r) eta[r] = eta_out_term[r];
     write_node<D, d>(o, e, tn, ls, eta, sig);
   }
+  BwdGrid bg(a.grid, a.first, e - 1);
   for (int64_t k = e - 1; k >= s; --k) {
     double tk[B], tki[B], ratio[B], pc[B][B];
-    M::taus(a.grid, a.first, k, tk, tki);
+    M::taus_h(bg.step(k), tk, tki);
 #pragma unroll
     for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
     M::phi_coefs(ratio, pc);
@@ -1041,6 +1064,7 @@ __global__ void __launch_bounds__(kLaneThreads, kBwdMinBlocks) k_lane_bwd_down(F
 #pragma unroll
       for (int r = 0; r < D; ++r) on[r] = eta_old[((e - 1 - s) * D + r) * nc + c];
     }
+    BwdGrid bg(a.grid, a.first, e - 1);
     for (int64_t k = e - 1; k >= s; --k) {
       double E[D][D], gk[D], oldk[D];
 #pragma unroll
@@ -1072,7 +1096,7 @@ __global__ void __launch_bounds__(kLaneThreads, kBwdMinBlocks) k_lane_bwd_down(F
         }
       }
       double tk[B], tki[B];
-      M::taus(a.grid, a.first, k, tk, tki);
+      M::taus_h(bg.step(k), tk, tki);
       double etak[D];
       if (kInitial) {
 #pragma unroll

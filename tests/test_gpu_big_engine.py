@@ -55,7 +55,21 @@ def test_pleiades_fixture(name):
     z = np.load(path)
     meta = json.loads(str(z["meta"]))
     got = gpu_solve(P, meta, max_iterations=meta["iterations"], **NEVER)
-    assert np.allclose(got.objective_trace, z["objective_trace"], rtol=1e-8)
+    # The objective after the first iteration from the constant start is a
+    # sum of whitened residuals x_{k+1} - phi x_k of nearly equal numbers:
+    # at N = 2^12 it is rounding-determined at ~1e-4 — the oracle's own
+    # seq_ieks and para_ieks (WorkPool(8), fixture *_par8_*) differ by 3.3e-4
+    # there.  Where that fixture exists the tolerance is twice the
+    # reference's own seq/par spread (never below 1e-8).
+    rtol = np.full(len(z["objective_trace"]), 1e-8)
+    alt = os.path.join(GOLDEN, name.replace("_seq_", "_par8_") + ".npz")
+    if os.path.exists(alt):
+        zp = np.load(alt)
+        spread = np.abs(zp["objective_trace"] - z["objective_trace"]) / np.abs(z["objective_trace"])
+        rtol = np.maximum(rtol, 2 * spread)
+    dev = np.abs(got.objective_trace - z["objective_trace"]) / np.abs(z["objective_trace"])
+    print(f"{name}: objective rel dev {dev}, tolerance {rtol}")
+    assert np.all(dev <= rtol)
     compare(got, z, meta, f"pleiades q3 N={meta['steps']} (fixture)", alternatives(P, meta, meta["iterations"]))
 
 

@@ -57,6 +57,7 @@ CASES = {
     "pleiades_q3_n10_seq": ("pleiades", 3, 10, 0, 100, False, 64),
     "pleiades_q3_n10_seq_it3": ("pleiades", 3, 10, 0, 3, True, 64),
     "pleiades_q3_n12_seq_it2": ("pleiades", 3, 12, 0, 2, True, 64),
+    "pleiades_q3_n12_par8_it2": ("pleiades", 3, 12, 8, 2, True, 64),
 }
 
 
