@@ -242,6 +242,17 @@ int pode_ieks(pode_context* ctx, const pode_problem* problem, const pode_prior* 
               const double* grid, int64_t n_nodes, const pode_ieks_config* config,
               pode_ieks_report* report, pode_status* status);
 
+/* Batched para_ieks (the reference solves one
+ * problem per call, ieks.cpp:114-217): `count` independent IVPs of one field
+ * kind and dimension (parameters and initial values free, e.g. a parameter
+ * sweep) sharing one prior, grid and config, fused into one pass sequence
+ * per Gauss-Newton iteration on the lane engine (d <= 3, D <= 9; else
+ * PODE_ERR_UNSUPPORTED).  Each IVP stops on its own by the reference's rule
+ * and reports[i] receives what pode_ieks would report for problems[i]. */
+int pode_ieks_batch(pode_context* ctx, const pode_problem* problems, int32_t count, const pode_prior* prior,
+                    const double* grid, int64_t n_nodes, const pode_ieks_config* config,
+                    pode_ieks_report* reports, pode_status* status);
+
 /* Replaces eks_solve (proj/include/paraode/ieks.hpp:103-105, ieks.cpp:224-291):
  * one forward pass linearised at each step's own predicted mean (sequential
  * in time: one warp on the device), the smoother of those filtered

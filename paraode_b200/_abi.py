@@ -101,6 +101,8 @@ SYMBOLS = {
                            C.POINTER(Status)]),
     "pode_ieks": (C.c_int, [C.c_void_p, C.POINTER(Problem), C.POINTER(Prior), dptr, C.c_int64,
                             C.POINTER(IeksConfig), C.POINTER(IeksReport), C.POINTER(Status)]),
+    "pode_ieks_batch": (C.c_int, [C.c_void_p, C.POINTER(Problem), C.c_int32, C.POINTER(Prior), dptr, C.c_int64,
+                                  C.POINTER(IeksConfig), C.POINTER(IeksReport), C.POINTER(Status)]),
     "pode_eks": (C.c_int, [C.c_void_p, C.POINTER(Problem), C.POINTER(Prior), dptr, C.c_int64, C.c_int32,
                            C.POINTER(IeksReport), C.POINTER(Status)]),
     "pode_rk4_table": (C.c_int, [C.c_void_p, C.POINTER(Problem), C.c_int64, dptr, C.POINTER(Status)]),

@@ -548,18 +548,73 @@ def eks_solve(ivp: InitialValueProblem, prior: IwpPrior, grid: Sequence[float], 
 _batch_pools: dict = {}  # device -> (lock, [Context]); a batch call holds its device's lock
 
 
+def para_ieks_fused_batch(problems: Sequence[InitialValueProblem], prior: IwpPrior, grid: Sequence[float],
+                          config: IeksConfig = IeksConfig(), want_cov=True, ctx=None):
+    """Many IVPs of one field kind and dimension (free parameters and initial
+    values, one prior / grid / config) solved as ONE fused solve on the
+    device (pode_ieks_batch): every Gauss-Newton iteration is one pass
+    sequence over all IVPs' time chunks, each IVP stopping on its own by the
+    reference's rule (ieks.cpp:157-187).  Report i is what para_ieks would
+    return for problems[i]."""
+    c = _ctx(ctx)
+    problems = list(problems)
+    if not problems:
+        return []
+    grid = _f64(grid)
+    n1 = grid.shape[0]
+    D, d = prior.state_dim, prior.dim
+    nb = len(problems)
+    outs, reps = [], (A.IeksReport * nb)()
+    for i in range(nb):
+        means = _result_array((n1, D))
+        cov = _result_array((n1, D, D)) if want_cov else None
+        sm = _result_array((n1, d))
+        sc = _result_array((n1, d, d)) if want_cov else None
+        trace = np.zeros(max(config.max_iterations, 1))
+        reps[i] = A.IeksReport(_p(means), _p(cov), _p(sm), _p(sc), _p(trace), trace.shape[0], A.PODE_HOST,
+                               0, 0, 0.0, A.ScanStats())
+        outs.append((means, cov, sm, sc, trace))
+    probs = (A.Problem * nb)()
+    keep = []  # the problems' y0/params buffers stay alive through the call
+    for i, p in enumerate(problems):
+        probs[i] = p._c()
+        keep.append(p)
+    prior_c = A.Prior(prior.nu, prior.dim, prior.sigma)
+    lin = {"ek1": 0, "ek0": 1}[config.linearization]
+    cfg = A.IeksConfig(config.max_iterations, config.traj_rtol, config.obj_atol, config.obj_rtol, lin)
+    st = A.Status()
+    _raise(c._lib.pode_ieks_batch(c.handle, probs, nb, C.byref(prior_c), _p(grid), n1, C.byref(cfg), reps,
+                                  C.byref(st)), st)
+    res = []
+    for i in range(nb):
+        means, cov, sm, sc, trace = outs[i]
+        r = reps[i]
+        res.append(SolverReport(grid.copy(), means, cov, sm, sc, r.sigma_hat, r.iterations,
+                                trace[:r.iterations].copy(), bool(r.converged),
+                                r.scan_stats.combine_invocations, r.scan_stats.sequential_depth))
+    return res
+
+
 def para_ieks_batch(problems: Sequence[InitialValueProblem], prior: IwpPrior, grid: Sequence[float],
-                    config: IeksConfig = IeksConfig(), want_cov=True, streams: int = 8, device: int = 0):
-    """Independent IVP solves (e.g. a parameter or initial-value sweep)
-    running concurrently: `streams` host threads, each driving its own
-    context (CUDA stream + workspace) through para_ieks, so small-N solves —
-    latency-bound one at a time — overlap on the GPU.  Returns the reports
-    in input order; each equals the single para_ieks call bit for bit
-    (SURVEY.md §8(f) item 4)."""
+                    config: IeksConfig = IeksConfig(), want_cov=True, streams: int = 8, device: int = 0,
+                    fused: bool = False):
+    """Independent IVP solves (e.g. a parameter or initial-value sweep).
+    fused=True: one fused device solve over all IVPs (para_ieks_fused_batch;
+    one field kind, lane engine).  Otherwise `streams` host threads, each
+    driving its own context (CUDA stream + workspace) through para_ieks, so
+    small-N solves — latency-bound one at a time — overlap on the GPU; each
+    report then equals the single para_ieks call bit for bit.  Reports are
+    in input order."""
     import threading
     problems = list(problems)
     if not problems:
         return []
+    if fused:
+        lock, ctxs = _batch_pools.setdefault(int(device), (threading.Lock(), []))
+        with lock:
+            if not ctxs:
+                ctxs.append(Context(device))
+            return para_ieks_fused_batch(problems, prior, grid, config, want_cov, ctx=ctxs[0])
     streams = max(1, min(int(streams), len(problems)))
     lock, ctxs = _batch_pools.setdefault(int(device), (threading.Lock(), []))
     with lock:  # contexts are not reentrant: one batch per device at a time

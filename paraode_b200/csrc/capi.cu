@@ -675,6 +675,74 @@ int pode_eks(pode_context* ctx, const pode_problem* problem, const pode_prior* p
   return solve_report(ctx, problem, prior, grid, n_nodes, &cfg, report, status, true);
 }
 
+int pode_ieks_batch(pode_context* ctx, const pode_problem* problems, int32_t count, const pode_prior* prior,
+                    const double* grid, int64_t n_nodes, const pode_ieks_config* config, pode_ieks_report* reports,
+                    pode_status* status) {
+  return guarded(status, [&] {
+    check_ctx(ctx);
+    if (problems == nullptr || prior == nullptr || grid == nullptr || config == nullptr || reports == nullptr)
+      throw ApiError(PODE_ERR_INVALID_INPUT, "ieks_batch: NULL argument");
+    if (count < 1) throw ApiError(PODE_ERR_INVALID_INPUT, "ieks_batch: need at least one problem");
+    if (config->max_iterations < 1) throw ApiError(PODE_ERR_INVALID_INPUT, "ieks: max_iterations must be at least 1");
+    if (prior->nu < 1 || prior->dim < 1) throw ApiError(PODE_ERR_INVALID_INPUT, "IwpPrior: need nu >= 1 and dim >= 1");
+    if (!(prior->sigma >= 0.0) || !std::isfinite(prior->sigma))
+      throw ApiError(PODE_ERR_INVALID_INPUT, "IwpPrior: sigma must be finite and nonnegative");
+    if (n_nodes < 2) throw ApiError(PODE_ERR_INVALID_INPUT, "discretize: grid needs at least two nodes");
+    if (grid[0] != 0.0) throw ApiError(PODE_ERR_INVALID_INPUT, "discretize: grid must start at t = 0");
+    check_grid_increasing(grid, n_nodes);
+    std::vector<host::Problem> ps;
+    ps.reserve(size_t(count));
+    for (int32_t i = 0; i < count; ++i) {
+      ps.push_back(host::resolve_problem(problems[i]));
+      if (ps.back().dim != prior->dim) throw ApiError(PODE_ERR_DIMENSION, "ieks: problem and prior dimensions disagree");
+    }
+    const int D = prior->dim * (prior->nu + 1);
+    const int d = prior->dim;
+    const EngineOps* ops = D <= kMaxD ? engine_ops(D) : nullptr;
+    if (ops == nullptr || ops->ieks_batch == nullptr)
+      throw ApiError(PODE_ERR_UNSUPPORTED, "ieks_batch: no batched engine for state dimension " + std::to_string(D));
+    const size_t n1 = size_t(n_nodes), nb = size_t(count);
+    bool want_cov = false, want_sm = false, want_sc = false;
+    for (size_t i = 0; i < nb; ++i) {
+      want_cov |= reports[i].cov_sqrt != nullptr;
+      want_sm |= reports[i].solution_means != nullptr;
+      want_sc |= reports[i].solution_covs != nullptr;
+    }
+    double* means = ctx->ws.arr<double>("bout_means", nb * n1 * D);
+    double* cov = want_cov ? ctx->ws.arr<double>("bout_cov", nb * n1 * D * D) : nullptr;
+    double* sm = want_sm ? ctx->ws.arr<double>("bout_sm", nb * n1 * d) : nullptr;
+    double* sc = want_sc ? ctx->ws.arr<double>("bout_sc", nb * n1 * d * d) : nullptr;
+    std::vector<IeksResult> rs;
+    if (!ops->ieks_batch(ctx, ps, *prior, grid, n_nodes, *config, means, cov, sm, sc, &rs))
+      throw ApiError(PODE_ERR_UNSUPPORTED, "ieks_batch: the batched engine needs d <= 3 and D <= 9");
+    raise_device_error(ctx, "ieks_batch: calibration");
+    for (size_t i = 0; i < nb; ++i) {
+      pode_ieks_report& rep = reports[i];
+      const bool dev = rep.location == PODE_DEVICE;
+      auto copy = [&](double* dst, const double* src, size_t n) {
+        if (dst == nullptr || src == nullptr) return;
+        if (dev)
+          cuda_check(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream),
+                     "ieks_batch outputs");
+        else
+          stage_out(ctx, dst, src, n, false);
+      };
+      copy(rep.means, means + i * n1 * D, n1 * D);
+      copy(rep.cov_sqrt, cov ? cov + i * n1 * D * D : nullptr, n1 * D * D);
+      copy(rep.solution_means, sm ? sm + i * n1 * d : nullptr, n1 * d);
+      copy(rep.solution_covs, sc ? sc + i * n1 * d * d : nullptr, n1 * d * d);
+      const IeksResult& r = rs[i];
+      rep.iterations = r.iterations;
+      rep.converged = r.converged ? 1 : 0;
+      rep.sigma_hat = r.sigma_hat;
+      rep.scan_stats = {r.stats.combines, r.stats.depth};
+      if (rep.objective_trace)
+        for (int k = 0; k < int(r.trace.size()) && k < rep.trace_capacity; ++k) rep.objective_trace[k] = r.trace[k];
+    }
+    cuda_check(cudaStreamSynchronize(ctx->stream), "ieks_batch sync");
+  });
+}
+
 int pode_rk4_table(pode_context* ctx, const pode_problem* problem, int64_t steps, double* table,
                    pode_status* status) {
   return guarded(status, [&] {

@@ -1,6 +1,8 @@
 // Runtime dispatch from the state dimension D to the compiled engine.
 #pragma once
 
+#include <vector>
+
 #include "context.hpp"
 
 namespace pode {
@@ -32,6 +34,10 @@ struct EngineOps {
   // eks_solve (element engine; cfg.linearization only)
   void (*eks)(pode_context*, const host::Problem&, const pode_prior&, const double*, int64_t,
               const pode_ieks_config&, double*, double*, double*, double*, IeksResult*);
+  // batched fused solve of many IVPs (batch_driver.cuh; lane engine only):
+  // outputs stacked per IVP, false when no batched engine serves (D, d)
+  bool (*ieks_batch)(pode_context*, const std::vector<host::Problem>&, const pode_prior&, const double*, int64_t,
+                     const pode_ieks_config&, double*, double*, double*, double*, std::vector<IeksResult>*);
 };
 
 // Shard s of R owns steps [floor(N s / R), floor(N (s+1) / R)).

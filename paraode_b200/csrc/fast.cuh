@@ -57,7 +57,36 @@ struct FastArgs {
   int first = 1;
   int last = 1;
   const double* carry = nullptr;  // D + D*D doubles
+  // Batch of independent IVPs (pode_ieks_batch, the kBatch kernels): IVP b
+  // owns chunks [b seg_chunks, (b+1) seg_chunks) of the chunk axis, the first
+  // seg_real of them real (N steps each, a shared grid), the rest padding up
+  // to whole lane blocks (identity aggregates, no output).  Every IVP's chunk
+  // 0 absorbs its own initial distribution, so the unsegmented aggregate
+  // scans restart at each IVP (a Gaussian element, A = 0, ignores its left
+  // operand; the terminal backward element, E = 0, its right operand).
+  int64_t seg_chunks = 0;
+  int64_t seg_real = 0;
+  const DevProblem* probs = nullptr;  // per IVP
+  const double* m0s = nullptr;        // per IVP: T_0^-1 mu_0 (D)
+  const int* active = nullptr;        // per IVP: still iterating (converged IVPs keep their buffers)
+  const int* seg_it = nullptr;        // finalize: per-IVP iteration count (its buffer parity)
 };
+
+// Position of chunk c on its IVP (kBatch) or on the single time axis.
+struct SegPos {
+  int64_t seg;    // IVP
+  int64_t cl;     // chunk index within the IVP
+  int64_t nreal;  // real chunks of the IVP
+};
+template <bool kBatch>
+__device__ __forceinline__ SegPos seg_pos(const FastArgs& a, int64_t c) {
+  if constexpr (kBatch) {
+    const int64_t b = c / a.seg_chunks;
+    return SegPos{b, c - b * a.seg_chunks, a.seg_real};
+  } else {
+    return SegPos{0, c, a.nchunks};
+  }
+}
 
 // The linearisation point of this iteration (its node-N slot in `term`).
 // Kernels keep their FastArgs parameter unmodified, so it stays in the
@@ -72,6 +101,22 @@ __device__ __forceinline__ LinPoint lin_point(const FastArgs& a) {
     return LinPoint{b, b + a.term_off};
   }
   return LinPoint{a.eta, a.eta_term};
+}
+// Batch: IVP seg's linearisation point (its node-N slot: term + seg D).  After
+// the loop (seg_it set) each IVP's own final point, pair[(it_b + 1) & 1].
+template <int D, bool kBatch>
+__device__ __forceinline__ LinPoint lin_point_seg(const FastArgs& a, int64_t seg) {
+  if constexpr (!kBatch) {
+    return lin_point(a);
+  } else {
+    int par;
+    if (a.seg_it != nullptr)
+      par = (a.seg_it[seg] + 1) & 1;
+    else
+      par = *a.it_dev & 1;
+    const double* b = par ? a.pair1 : a.pair0;
+    return LinPoint{b, b + a.term_off + seg * D};
+  }
 }
 
 __device__ __forceinline__ double ipow(double h, int k) {

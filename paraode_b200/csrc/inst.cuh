@@ -5,6 +5,7 @@
 
 #include "dispatch.hpp"
 #include "fast_driver.cuh"
+#include "batch_driver.cuh"
 #include "ieks.cuh"
 
 #ifndef PODE_D
@@ -117,7 +118,34 @@ void ek(pode_context* c, const host::Problem& p, const pode_prior& pr, const dou
         const pode_ieks_config& cfg, double* m, double* cv, double* sm, double* sc, IeksResult* out) {
   *out = IeksEngine<kD>::run_eks(c, p, pr, g, n1, cfg, m, cv, sm, sc);
 }
-const EngineOps kOps{kD, cf, cs, mf, ms, sf, ss, rt, ik, iks, ek};
+// Batched fused solve: the lane engine's kBatch passes.
+bool ikb(pode_context* c, const std::vector<host::Problem>& ps, const pode_prior& pr, const double* g, int64_t n1,
+         const pode_ieks_config& cfg, double* m, double* cv, double* sm, double* sc, std::vector<IeksResult>* out) {
+  switch (pr.dim) {
+    case 1:
+      if constexpr (kFastOk<kD, 1>) {
+        *out = BatchEngine<kD, 1>::run(c, ps, pr, g, n1, cfg, m, cv, sm, sc);
+        return true;
+      }
+      break;
+    case 2:
+      if constexpr (kFastOk<kD, 2>) {
+        *out = BatchEngine<kD, 2>::run(c, ps, pr, g, n1, cfg, m, cv, sm, sc);
+        return true;
+      }
+      break;
+    case 3:
+      if constexpr (kFastOk<kD, 3>) {
+        *out = BatchEngine<kD, 3>::run(c, ps, pr, g, n1, cfg, m, cv, sm, sc);
+        return true;
+      }
+      break;
+    default:
+      break;
+  }
+  return false;
+}
+const EngineOps kOps{kD, cf, cs, mf, ms, sf, ss, rt, ik, iks, ek, ikb};
 }  // namespace
 
 const EngineOps* PODE_CAT(engine_ops_d, PODE_D)() { return &kOps; }

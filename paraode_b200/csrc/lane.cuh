@@ -439,25 +439,43 @@ __device__ __forceinline__ void block_sum_partial(double* red, double v, double*
 // ------------------------------------------------------------- pass A ---
 // One thread per chunk: fold the chunk's filtering elements into the
 // aggregate (A, b, C, eta, J) (see fast.cuh for the algebra).
-template <int D, int d>
+template <int D, int d, bool kBatch = false>
 __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks) k_lane_fwd_reduce(const FastArgs a, FastConst<D> cst, FEd agg) {
   using M = Model<D, d>;
   constexpr int B = M::B;
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (c >= a.nchunks) return;
-  const LinPoint lp = lin_point(a);
-  const int64_t s = c * a.L;
+  const SegPos sp = seg_pos<kBatch>(a, c);
+  if (kBatch && sp.cl >= sp.nreal) {  // padding chunk: the identity aggregate
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        agg.a[c * D * D + r * D + j] = (r == j) ? 1.0 : 0.0;
+        agg.c[c * D * D + r * D + j] = 0.0;
+        agg.j[c * D * D + r * D + j] = 0.0;
+      }
+      agg.b[c * D + r] = 0.0;
+      agg.eta[c * D + r] = 0.0;
+    }
+    return;
+  }
+  if (kBatch && a.active != nullptr && !a.active[sp.seg]) return;  // converged IVP: its aggregates are not read
+  const LinPoint lp = lin_point_seg<D, kBatch>(a, sp.seg);
+  const DevProblem& prob = kBatch ? a.probs[sp.seg] : a.prob;
+  const bool head = sp.cl == 0 && a.first;
+  const int64_t s = sp.cl * a.L;
   const int64_t e = min(a.N, s + a.L);
   double A[D][D], C[D][D], J[D][D], b[D], eta[D];
 #pragma unroll
   for (int r = 0; r < D; ++r) {
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      A[r][j] = (!(c == 0 && a.first) && r == j) ? 1.0 : 0.0;
+      A[r][j] = (!head && r == j) ? 1.0 : 0.0;
       C[r][j] = 0.0;
       J[r][j] = 0.0;
     }
-    b[r] = (c == 0 && a.first) ? cst.m0[r] : 0.0;
+    b[r] = head ? (kBatch ? a.m0s[sp.seg * D + r] : cst.m0[r]) : 0.0;
     eta[r] = 0.0;
   }
   double tk[B], tki[B];
@@ -483,7 +501,7 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks) k_lane_fwd_reduc
     // update at node k+1
     double ylin[d];  // (a one-step-ahead load costs pass A more in spills than it saves)
     gather_y<D, d>(a, lp, c, k + 1 - s, k + 1, ylin);
-    const typename M::Lin lin = M::linearize(a.prob, ylin, a.ek0, a.prob.kind == 7 ? a.grid[k + 1] : 0.0);
+    const typename M::Lin lin = M::linearize(prob, ylin, a.ek0, prob.kind == 7 ? a.grid[k + 1] : 0.0);
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
     const typename M::Upd u = M::update(lin, tn, cm);
     bad_sing |= u.singular;
@@ -573,25 +591,26 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks) k_lane_fwd_reduc
 // of every node (cf, chunk-interleaved like E; node N in cterm) and reduces
 // the whitened innovations ||S^-1 (H m- - offset)||^2 (innovation_stats,
 // ieks.cpp:79-104) into one partial per block.
-template <int D, int d, bool kFinal>
+template <int D, int d, bool kFinal, bool kBatch>
 __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastConst<D>& cst, const FEd& prefix,
                                                  const ElemSoA& elems, double* cf, double* cterm, int64_t c,
-                                                 double* sacc, const SEd& bagg) {
+                                                 double* sacc, const SEd& bagg, const SegPos& sp) {
   using M = Model<D, d>;
   constexpr int B = M::B;
   double innov = 0.0;
-  const LinPoint lp = lin_point(a);
-  const int64_t s = c * a.L;
+  const LinPoint lp = lin_point_seg<D, kBatch>(a, sp.seg);
+  const DevProblem& prob = kBatch ? a.probs[sp.seg] : a.prob;
+  const int64_t s = sp.cl * a.L;
   const int64_t e = min(a.N, s + a.L);
   double m[D], C[D][D];
-  if (c == 0 && a.first) {
+  if (sp.cl == 0 && a.first) {
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-      m[r] = cst.m0[r];
+      m[r] = kBatch ? a.m0s[sp.seg * D + r] : cst.m0[r];
 #pragma unroll
       for (int j = 0; j < D; ++j) C[r][j] = 0.0;
     }
-  } else if (c == 0) {  // shard > 0: the filtered marginal folded from the left
+  } else if (sp.cl == 0) {  // shard > 0: the filtered marginal folded from the left
     ld_mat<D>(a.carry + D, C);
 #pragma unroll
     for (int r = 0; r < D; ++r) m[r] = a.carry[r];
@@ -714,7 +733,7 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
 #pragma unroll
     for (int i = 0; i < d; ++i) ylin[i] = ynext[i];
     if (k + 1 < e) gather_y<D, d>(a, lp, c, k + 2 - s, k + 2, ynext);
-    const typename M::Lin lin = M::linearize(a.prob, ylin, a.ek0, a.prob.kind == 7 ? a.grid[k + 1] : 0.0);
+    const typename M::Lin lin = M::linearize(prob, ylin, a.ek0, prob.kind == 7 ? a.grid[k + 1] : 0.0);
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
     const typename M::Upd u = M::update(lin, tn, cm);
     bad_sing |= u.singular;
@@ -745,8 +764,8 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
   }
   if (e == a.N) {  // terminal node N: E = 0, g = m_f(N) (parallel.cpp:137-144)
 #pragma unroll
-    for (int r = 0; r < D; ++r) elems.term[r] = m[r];
-    if constexpr (kFinal) st_mat<D>(cterm, C);
+    for (int r = 0; r < D; ++r) elems.term[sp.seg * D + r] = m[r];
+    if constexpr (kFinal) st_mat<D>(cterm + sp.seg * D * D, C);
   }
   if constexpr (!kFinal) {  // store the backward aggregate (the last shard's last chunk absorbs the terminal)
     const bool term = e == a.N && a.last;
@@ -770,7 +789,7 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
   return innov;
 }
 
-template <int D, int d, bool kFinal = false>
+template <int D, int d, bool kFinal = false, bool kBatch = false>
 __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks) k_lane_fwd_down(const FastArgs a, FastConst<D> cst, FEd prefix,
                                                                 ElemSoA elems, double* cf = nullptr,
                                                                 double* cterm = nullptr, double* part = nullptr,
@@ -779,7 +798,21 @@ __global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks) k_lane_fwd_down(
   extern __shared__ double sacc[];  // !kFinal: (D*D + D) x kLaneThreads aggregate slots
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   double innov = 0.0;
-  if (c < a.nchunks) innov = fwd_down_chunk<D, d, kFinal>(a, cst, prefix, elems, cf, cterm, c, sacc, bagg);
+  if (c < a.nchunks) {
+    const SegPos sp = seg_pos<kBatch>(a, c);
+    if (kBatch && sp.cl >= sp.nreal) {  // padding chunk: identity backward aggregate
+      if constexpr (!kFinal) {
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+#pragma unroll
+          for (int j = 0; j < D; ++j) bagg.e[c * D * D + r * D + j] = (r == j) ? 1.0 : 0.0;
+          bagg.g[c * D + r] = 0.0;
+        }
+      }
+    } else if (!kBatch || a.active == nullptr || a.active[sp.seg]) {
+      innov = fwd_down_chunk<D, d, kFinal, kBatch>(a, cst, prefix, elems, cf, cterm, c, sacc, bagg, sp);
+    }
+  }
   if constexpr (kFinal) block_sum_partial(red, innov, part);  // every thread reaches the barriers
 }
 
@@ -844,24 +877,37 @@ __device__ __forceinline__ void smooth_combine_factor(const double (&E)[D][D], c
 // F2: each chunk's full smoothing aggregate e_s ⊗ .. ⊗ e_{e-1} (⊗ the
 // terminal element for the last chunk) as (E, g, L), folded backwards; the
 // per-node L_k are formed on the fly from (E_k, C_f(k)).
-template <int D, int d>
+template <int D, int d, bool kBatch = false>
 __global__ void __launch_bounds__(kLaneThreads) k_lane_fin_fold(FastArgs a, FastConst<D> cst, ElemSoA elems,
                                                                 const double* cf, const double* cterm, SEd agg) {
   using M = Model<D, d>;
   constexpr int B = M::B;
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (c >= a.nchunks) return;
-  const int64_t s = c * a.L;
+  const SegPos sp = seg_pos<kBatch>(a, c);
+  if (kBatch && sp.cl >= sp.nreal) {  // padding chunk: the identity (E, g, L) = (I, 0, 0)
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        agg.e[c * D * D + r * D + j] = (r == j) ? 1.0 : 0.0;
+        agg.l[c * D * D + r * D + j] = 0.0;
+      }
+      agg.g[c * D + r] = 0.0;
+    }
+    return;
+  }
+  const int64_t s = sp.cl * a.L;
   const int64_t e = min(a.N, s + a.L);
-  const bool last = c == a.nchunks - 1 && a.last;
+  const bool last = sp.cl == sp.nreal - 1 && a.last;
   double ea[D][D], la[D][D], ga[D];
 #pragma unroll
   for (int r = 0; r < D; ++r) {
-    ga[r] = last ? elems.term[r] : 0.0;
+    ga[r] = last ? elems.term[sp.seg * D + r] : 0.0;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       ea[r][j] = (!last && r == j) ? 1.0 : 0.0;
-      la[r][j] = last ? cterm[r * D + j] : 0.0;
+      la[r][j] = last ? cterm[sp.seg * D * D + r * D + j] : 0.0;
     }
   }
   double tn[B], tni[B];
@@ -954,7 +1000,7 @@ __device__ __forceinline__ void write_node(const FinOut& o, int64_t n, const dou
 // F4: backward smoothed-factor recursion L^s_k = tria([E_k L^s_{k+1}, L_k])
 // from each chunk's incoming factor (the reverse scan of the F2 aggregates;
 // the last chunk starts from C_f(N)), fused with the output projection.
-template <int D, int d>
+template <int D, int d, bool kBatch = false>
 __global__ void __launch_bounds__(kLaneThreads) k_lane_fin_bwd(FastArgs a, FastConst<D> cst, ElemSoA elems,
                                                                const double* cf, const double* cterm, SEd suffix,
                                                                const double* eta_out, const double* eta_out_term,
@@ -963,19 +1009,26 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fin_bwd(FastArgs a, FastC
   constexpr int B = M::B;
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (c >= a.nchunks) return;
-  const int64_t s = c * a.L;
+  const SegPos sp = seg_pos<kBatch>(a, c);
+  if (kBatch && sp.cl >= sp.nreal) return;
+  if constexpr (kBatch) {  // IVP seg's newest trajectory: pair[it_b & 1]
+    eta_out = (a.seg_it[sp.seg] & 1) ? a.pair1 : a.pair0;
+    eta_out_term = eta_out + a.term_off + sp.seg * D;
+  }
+  const int64_t s = sp.cl * a.L;
   const int64_t e = min(a.N, s + a.L);
-  const bool last = c == a.nchunks - 1;  // cterm: C_f(N), or the right carry's factor (shards)
-  const double sig = sqrt(innov[0] / count);
+  const int64_t out0 = sp.seg * (a.N + 1);  // output node offset of this IVP
+  const bool last = sp.cl == sp.nreal - 1;  // cterm: C_f(N), or the right carry's factor (shards)
+  const double sig = sqrt(innov[sp.seg] / count);
   double ls[D][D];
-  ld_mat<D>(last ? cterm : suffix.l + (c + 1) * D * D, ls);
+  ld_mat<D>(last ? cterm + sp.seg * D * D : suffix.l + (c + 1) * D * D, ls);
   double tn[B], tni[B];
   M::taus(a.grid, a.first, e, tn, tni);
   if (last && a.last) {
     double eta[D];
 #pragma unroll
     for (int r = 0; r < D; ++r) eta[r] = eta_out_term[r];
-    write_node<D, d>(o, e, tn, ls, eta, sig);
+    write_node<D, d>(o, out0 + e, tn, ls, eta, sig);
   }
   BwdGrid bg(a.grid, a.first, e - 1);
   for (int64_t k = e - 1; k >= s; --k) {
@@ -992,7 +1045,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fin_bwd(FastArgs a, FastC
     double eta[D];
 #pragma unroll
     for (int r = 0; r < D; ++r) eta[r] = eta_out[((k - s) * D + r) * a.nchunks + c];
-    write_node<D, d>(o, k, tk, ls, eta, sig);
+    write_node<D, d>(o, out0 + k, tk, ls, eta, sig);
 #pragma unroll
     for (int i = 0; i < B; ++i) {
       tn[i] = tk[i];
@@ -1008,7 +1061,7 @@ __global__ void __launch_bounds__(kLaneThreads) k_lane_fin_bwd(FastArgs a, FastC
 // eta_old / eta_new (and their node-N slots) are in the chunk-interleaved
 // layout of eta_at; the next step's (E, g, eta_old) are prefetched while the
 // current step computes.
-template <int D, int d, bool kInitial>
+template <int D, int d, bool kInitial, bool kBatch = false>
 __global__ void __launch_bounds__(kLaneThreads, kBwdMinBlocks) k_lane_bwd_down(FastArgs a, FastConst<D> cst, ElemSoA elems,
                                                                 SEd suffix, const double* eta_old,
                                                                 const double* old_term, double* eta_new,
@@ -1017,8 +1070,9 @@ __global__ void __launch_bounds__(kLaneThreads, kBwdMinBlocks) k_lane_bwd_down(F
   constexpr int B = M::B;
   __shared__ double red[3][kLaneThreads];
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  const bool okc = c < a.nchunks;
   const int64_t nc = a.nchunks;
+  const SegPos sp = seg_pos<kBatch>(a, c < nc ? c : nc - 1);
+  const bool okc = c < nc && (!kBatch || (sp.cl < sp.nreal && a.active[sp.seg]));
   double obj = 0.0, dmax = 0.0, emax = 0.0;
   if (a.it_dev != nullptr) {  // graph-loop mode: buffers by iteration parity
     const int par = *a.it_dev & 1;
@@ -1028,21 +1082,25 @@ __global__ void __launch_bounds__(kLaneThreads, kBwdMinBlocks) k_lane_bwd_down(F
     new_term = eta_new + a.term_off;
   }
   if (okc) {
-    const int64_t s = c * a.L;
+    if constexpr (kBatch) {  // this IVP's node-N slots
+      old_term += sp.seg * D;
+      new_term += sp.seg * D;
+    }
+    const int64_t s = sp.cl * a.L;
     const int64_t e = min(a.N, s + a.L);
-    const bool last = c == a.nchunks - 1;
+    const bool last = sp.cl == sp.nreal - 1;
     double mu[D], te[B], tei[B];
     M::taus(a.grid, a.first, e, te, tei);
     double bar_next[D];
 #pragma unroll
     for (int r = 0; r < D; ++r) {
       double eta_e;
-      const double old_e = eta_at<D>(eta_old, old_term, e, r, a.N, a.L, nc);
+      const double old_e = (e == a.N) ? old_term[r] : eta_old[r * nc + c + 1];  // the next chunk's node 0
       if (kInitial) {
         eta_e = old_e;
         mu[r] = 0.0;
       } else {
-        mu[r] = last ? elems.term[r] : suffix.g[(c + 1) * D + r];
+        mu[r] = last ? elems.term[sp.seg * D + r] : suffix.g[(c + 1) * D + r];
         eta_e = te[r % B] * mu[r];
       }
       if (last) {

@@ -67,6 +67,8 @@ def test_no_gpu_fails_loudly_without_fallback():
         P.eks_solve(P.logistic(), P.IwpPrior(1, 1, 1.0), P.uniform_grid(10.0, 16))
     with pytest.raises(P.CudaError):
         P.para_ieks_batch([P.logistic()] * 3, P.IwpPrior(1, 1, 1.0), P.uniform_grid(10.0, 16))
+    with pytest.raises(P.CudaError):
+        P.para_ieks_batch([P.logistic()] * 3, P.IwpPrior(1, 1, 1.0), P.uniform_grid(10.0, 16), fused=True)
     from paraode_b200.accuracy import rk4_table
     with pytest.raises(P.CudaError):
         rk4_table(P.rigid_body(), 64)
