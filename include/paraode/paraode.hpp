@@ -456,6 +456,20 @@ inline RtsResult seq_rts(const GaussianSqrt& init, const std::vector<TransitionM
 
 // --------------------------------------------------------------- ieks ---
 namespace detail {
+// Host output buffers of one pode_ieks_report and their conversion to SolverReport.
+struct ReportBuf {
+  std::vector<double> means, cov, sm, sc, trace;
+  pode_ieks_report rep;
+  ReportBuf(Index n1, Index D, Index d, int max_iterations)
+      : means(size_t(n1 * D)), cov(size_t(n1 * D * D)), sm(size_t(n1 * d)), sc(size_t(n1 * d * d)),
+        trace(size_t(std::max(max_iterations, 1))),
+        rep{means.data(), cov.data(), sm.data(), sc.data(), trace.data(), int32_t(trace.size()), PODE_HOST, 0, 0,
+            0.0, {0, 0}} {}
+  ReportBuf(const ReportBuf&) = delete;
+  ReportBuf& operator=(const ReportBuf&) = delete;
+  SolverReport report(const std::vector<double>& grid, Index D, Index d) const;
+};
+
 inline SolverReport ieks(const InitialValueProblem& ivp, const IwpPrior& prior, const std::vector<double>& grid,
                          const IeksConfig& config, WorkPool& pool, bool eks, int64_t chunk) {
   if (!ivp.registered.valid)
@@ -471,16 +485,31 @@ inline SolverReport ieks(const InitialValueProblem& ivp, const IwpPrior& prior, 
   pode_prior pr{prior.nu, prior.dim, prior.sigma};
   const int lin = config.linearization == Linearization::kEk0 ? 1 : 0;
   pode_ieks_config cfg{config.max_iterations, config.traj_rtol, config.obj_atol, config.obj_rtol, lin};
-  std::vector<double> means(size_t(n1 * D)), cov(size_t(n1 * D * D)), sm(size_t(n1 * d)), sc(size_t(n1 * d * d));
-  std::vector<double> trace(size_t(std::max(config.max_iterations, 1)));
-  pode_ieks_report rep{means.data(), cov.data(), sm.data(), sc.data(), trace.data(), int32_t(trace.size()),
-                       PODE_HOST, 0, 0, 0.0, {0, 0}};
+  ReportBuf b(n1, D, d, config.max_iterations);
   pode_status st{};
   pode_context_set_option(pool.handle(), PODE_OPT_CHUNK_LEN, chunk);
-  const int rc = eks ? pode_eks(pool.handle(), &p, &pr, grid.data(), n1, lin, &rep, &st)
-                     : pode_ieks(pool.handle(), &p, &pr, grid.data(), n1, &cfg, &rep, &st);
+  const int rc = eks ? pode_eks(pool.handle(), &p, &pr, grid.data(), n1, lin, &b.rep, &st)
+                     : pode_ieks(pool.handle(), &p, &pr, grid.data(), n1, &cfg, &b.rep, &st);
   pode_context_set_option(pool.handle(), PODE_OPT_CHUNK_LEN, 0);
   check(rc, st);
+  return b.report(grid, D, d);
+}
+
+inline pode_problem registered(const InitialValueProblem& ivp, std::vector<double>& y0) {
+  if (!ivp.registered.valid)
+    throw InvalidInputError("ieks: the problem has only host callbacks; the B200 path needs a registered device "
+                            "field (InitialValueProblem::registered) — there is no CPU fallback");
+  y0.resize(size_t(ivp.dim));
+  putv(ivp.y0, y0.data(), ivp.dim);
+  return pode_problem{int32_t(ivp.registered.kind), ivp.dim, ivp.t_end, y0.data(),
+                      ivp.registered.params.empty() ? nullptr : ivp.registered.params.data(),
+                      int32_t(ivp.registered.params.size())};
+}
+}  // namespace detail
+
+namespace detail {
+inline SolverReport ReportBuf::report(const std::vector<double>& grid, Index D, Index d) const {
+  const Index n1 = Index(grid.size());
   SolverReport out;
   out.times = grid;
   out.marginals.resize(size_t(n1));
@@ -521,6 +550,41 @@ inline SolverReport eks_solve(const InitialValueProblem& ivp, const IwpPrior& pr
   IeksConfig cfg;
   cfg.linearization = linearization;
   return detail::ieks(ivp, prior, grid, cfg, detail::default_pool(), true, 0);
+}
+
+// Batched para_ieks (no reference counterpart — the reference solves one IVP
+// per call): IVPs of one registered field kind and
+// dimension with one prior, grid and config, fused into one device solve
+// (pode_ieks_batch).  Element i equals para_ieks(ivps[i], ...) at the
+// reference's tolerances, with its own iteration count.
+inline std::vector<SolverReport> para_ieks_batch(const std::vector<InitialValueProblem>& ivps, const IwpPrior& prior,
+                                                 const std::vector<double>& grid, const IeksConfig& config,
+                                                 WorkPool& pool) {
+  const Index D = prior.state_dim(), d = prior.dim, n1 = Index(grid.size());
+  std::vector<std::vector<double>> y0(ivps.size());
+  std::vector<pode_problem> ps;
+  std::vector<std::unique_ptr<detail::ReportBuf>> bufs;
+  std::vector<pode_ieks_report> reps;
+  for (size_t i = 0; i < ivps.size(); ++i) {
+    if (ivps[i].dim != prior.dim) throw DimensionError("ieks: problem and prior dimensions disagree");
+    ps.push_back(detail::registered(ivps[i], y0[i]));
+    bufs.push_back(std::make_unique<detail::ReportBuf>(n1, D, d, config.max_iterations));
+    reps.push_back(bufs.back()->rep);
+  }
+  if (ps.empty()) return {};
+  pode_prior pr{prior.nu, prior.dim, prior.sigma};
+  const int lin = config.linearization == Linearization::kEk0 ? 1 : 0;
+  pode_ieks_config cfg{config.max_iterations, config.traj_rtol, config.obj_atol, config.obj_rtol, lin};
+  pode_status st{};
+  detail::check(pode_ieks_batch(pool.handle(), ps.data(), int32_t(ps.size()), &pr, grid.data(), n1, &cfg,
+                                reps.data(), &st),
+                st);
+  std::vector<SolverReport> out;
+  for (size_t i = 0; i < ps.size(); ++i) {
+    bufs[i]->rep = reps[i];  // iterations, convergence, sigma-hat
+    out.push_back(bufs[i]->report(grid, D, d));
+  }
+  return out;
 }
 
 // ----------------------------------------------------------- problems ---

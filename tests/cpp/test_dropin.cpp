@@ -213,6 +213,24 @@ static void sequential_and_parallel_agree() {  // test_ieks.cpp:248-269
   CHECK(eks.iterations == 1 && eks.converged);
 }
 
+static void batch_matches_single_solves() {  // para_ieks_batch
+  WorkPool pool;
+  std::vector<InitialValueProblem> ivps;
+  for (double mu : {0.5, 1.0, 2.0}) ivps.push_back(van_der_pol(mu).ivp);
+  const std::vector<double> grid = uniform_grid(6.3, 150);
+  const std::vector<SolverReport> batch = para_ieks_batch(ivps, IwpPrior{2, 2, 1.0}, grid, IeksConfig{}, pool);
+  CHECK(batch.size() == ivps.size());
+  for (size_t i = 0; i < ivps.size(); ++i) {
+    const SolverReport one = para_ieks(ivps[i], IwpPrior{2, 2, 1.0}, grid, IeksConfig{}, pool);
+    CHECK(batch[i].iterations == one.iterations && batch[i].converged == one.converged);
+    double dm = 0.0;
+    for (size_t n = 0; n < grid.size(); ++n)
+      dm = std::max(dm, max_abs_diff(batch[i].marginals[n].mean, one.marginals[n].mean));
+    CHECK(dm <= 1e-9);
+    CHECK(std::fabs(batch[i].sigma_hat - one.sigma_hat) <= 1e-7 * std::fabs(one.sigma_hat));
+  }
+}
+
 static void logistic_matches_the_closed_form() {  // test_ieks.cpp:271-282 / acceptance.cpp:167-179
   WorkPool pool;
   const NamedProblem p = logistic();
@@ -284,6 +302,7 @@ int main() {
   arbitrary_scan_operators_do_not_run();
   affine_converges_in_two_iterations();
   sequential_and_parallel_agree();
+  batch_matches_single_solves();
   logistic_matches_the_closed_form();
   invariant_under_sigma_and_budget();
   host_only_callbacks_are_rejected();
@@ -292,6 +311,6 @@ int main() {
     std::printf("%d failures\n", failures);
     return 1;
   }
-  std::printf("PASS (drop-in header, 12 reference-style cases)\n");
+  std::printf("PASS (drop-in header, 12 reference-style cases + the batched solve)\n");
   return 0;
 }
