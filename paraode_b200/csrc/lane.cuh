@@ -24,7 +24,10 @@
 namespace pode {
 namespace lane {
 
-constexpr int kLaneThreads = 128;
+#ifndef PODE_LANE_THREADS
+#define PODE_LANE_THREADS 128
+#endif
+constexpr int kLaneThreads = PODE_LANE_THREADS;
 // Pass E is HBM-bound: more resident warps would keep more loads in flight
 // (register cap 64K / (128 * kBwdMinBlocks)); 3 and 4 spilled, so 2.
 #ifndef PODE_BWD_MIN_BLOCKS
@@ -37,6 +40,13 @@ constexpr int kBwdMinBlocks = PODE_BWD_MIN_BLOCKS;
 #define PODE_LANE_MIN_BLOCKS 1
 #endif
 constexpr int kLaneMinBlocks = PODE_LANE_MIN_BLOCKS;
+// Register budget of passes A and C: the launch bounds above, or an explicit
+// cap (PODE_LANE_MAXNREG, developer A/B builds).
+#ifdef PODE_LANE_MAXNREG
+#define PODE_LANE_BOUNDS __maxnreg__(PODE_LANE_MAXNREG)
+#else
+#define PODE_LANE_BOUNDS __launch_bounds__(kLaneThreads, kLaneMinBlocks)
+#endif
 
 // Householder LQ of an R x K row-major register matrix over the first P
 // pivots: row p is reflected against columns p..K-1 and every later row is
@@ -440,7 +450,7 @@ __device__ __forceinline__ void block_sum_partial(double* red, double v, double*
 // One thread per chunk: fold the chunk's filtering elements into the
 // aggregate (A, b, C, eta, J) (see fast.cuh for the algebra).
 template <int D, int d, bool kBatch = false>
-__global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks) k_lane_fwd_reduce(const FastArgs a, FastConst<D> cst, FEd agg) {
+__global__ void PODE_LANE_BOUNDS k_lane_fwd_reduce(const FastArgs a, FastConst<D> cst, FEd agg) {
   using M = Model<D, d>;
   constexpr int B = M::B;
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -790,7 +800,7 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
 }
 
 template <int D, int d, bool kFinal = false, bool kBatch = false>
-__global__ void __launch_bounds__(kLaneThreads, kLaneMinBlocks) k_lane_fwd_down(const FastArgs a, FastConst<D> cst, FEd prefix,
+__global__ void PODE_LANE_BOUNDS k_lane_fwd_down(const FastArgs a, FastConst<D> cst, FEd prefix,
                                                                 ElemSoA elems, double* cf = nullptr,
                                                                 double* cterm = nullptr, double* part = nullptr,
                                                                 SEd bagg = SEd{}) {
