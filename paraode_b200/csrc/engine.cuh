@@ -490,6 +490,10 @@ struct FTOps : FOps<D> {
   }
 };
 
+}  // namespace pode
+#include "wide.cuh"  // wide groups (2D lanes per element) for the latency-bound upper scan levels
+namespace pode {
+
 // ---------------------------------------- block (Sklansky) local scans ---
 // The upper levels of the aggregate scans are latency-bound chains of
 // combines.  Here one CTA of kBWarps warps scans G = kBWarps * (32 / D)
@@ -562,6 +566,18 @@ constexpr bool bscan_fits() {
 // Scan levels above 0 with at most this many elements use the block kernel
 // (latency-bound: Sklansky depth); larger levels keep the work-efficient
 // sequential fan-in (throughput-bound).  PODE_BSCAN=0 disables, =n sets it.
+// Upper ⊗_f scan levels on wide groups (wide.cuh) when PODE_WIDE=1.  Off by
+// default: per iteration at N = 2^20 (tools/prof_events.py, block-scan time)
+// it is neutral at D = 2 / 6 (-1 / -3 %), slower at D = 8 (+8 %) and faster
+// only where the scan is a small share of the iteration (D = 4: -15 %,
+// D = 9: -17 %, D = 12: -40 %; whole iterations within 0.6 %).  The per-pivot
+// broadcast of the 2D-wide pivot row and its redundant reflector — not the
+// row updates that the wide layout halves — set the combine's latency.
+inline bool bscan_wide() {
+  const char* env = std::getenv("PODE_WIDE");
+  return env != nullptr && *env != '\0' && std::atoi(env) == 1;
+}
+
 inline int64_t bscan_max() {
   const char* env = std::getenv("PODE_BSCAN");
   if (env == nullptr || *env == '\0') return 16384;  // tools/knob_sweep.py (ms per iteration)
@@ -671,6 +687,32 @@ struct Engine {
     DevError* err = reinterpret_cast<DevError*>(ctx->d_err);
     size_t sm = smem_bytes<D>();
     FEd loc = alloc<FOps<D>>(ctx, "gscan_loc_" + std::to_string(level), n);
+    if constexpr (2 * D <= 32 && bscan_smem_w<D>() <= size_t(227) * 1024) {
+      if (level >= 1 && n <= bscan_max() && bscan_wide()) {  // block Sklansky levels, wide groups
+        constexpr int G = bscan_groups_w<D>();
+        sm = bscan_smem_w<D>();
+        static OncePerDevice once;
+        once([&] {
+          cuda_check(cudaFuncSetAttribute(k_bscan_loc_w<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)),
+                     "bscan smem");
+        });
+        const int64_t nb = (n + G - 1) / G;
+        FEd agg = alloc<FOps<D>>(ctx, "gscan_agg_" + std::to_string(level), nb);
+        k_bscan_loc_w<D><<<unsigned(nb), kBWarpsW * 32, sm, ctx->stream>>>(in, n, nb == 1 ? out : loc, agg, err);
+        note_launch(ctx, "bscan_g");
+        int depth = 0;
+        while ((1 << depth) < std::min<int64_t>(n, G)) ++depth;
+        t.depth += depth;
+        t.combines += n * depth;
+        if (nb == 1) return;
+        scan_gauss_rec(ctx, agg, agg, nb, level + 1, L, t);
+        k_scan_down_gauss<D><<<blocks_for<D>(n), kThreads, smem_bytes<D>(), ctx->stream>>>(loc, n, G, agg, out, err);
+        note_launch(ctx, "scan_g_down");
+        t.combines += n - std::min<int64_t>(n, G);
+        t.depth += 1;
+        return;
+      }
+    }
     if (level >= 1 && n <= bscan_max() && bscan_fits<D, FOps<D>>()) {  // block Sklansky levels
       constexpr int G = bscan_groups<D>();
       sm = bscan_smem<D, FOps<D>>();

@@ -324,6 +324,22 @@ def test_ek0_matches_oracle():  # statespace.cpp:90-103
     assert rel(got.means, want["means"]) <= 1e-9
 
 
+@pytest.mark.parametrize("name,nu,n", [("fhn", 2, 4000), ("vanderpol", 2, 3000), ("rigidbody", 2, 3000)])
+def test_wide_group_block_scans_match_oracle(name, nu, n, monkeypatch):
+    """The opt-in wide-group upper scan levels (PODE_WIDE=1, wide.cuh) give
+    the oracle's iterates (short chunks force several block-scan levels)."""
+    monkeypatch.setenv("PODE_WIDE", "1")
+    prob = P.problem_by_name(name)
+    grid = O.uniform_grid(prob.t_end, n)
+    ctx = P.Context()
+    ctx.set_chunk_len(2)
+    got = P.para_ieks(prob, P.IwpPrior(nu, prob.dim, 1.0), grid, ctx=ctx)
+    want = O.ieks(_orc_problem(name), nu, grid, mode=0)
+    assert got.iterations == want["iterations"]
+    assert rel(got.means, want["means"]) <= 1e-9
+    assert rel(dense_cov(got.cov_sqrt), dense_cov(want["cov_sqrt"])) <= 1e-7
+
+
 def test_ragged_grid_matches_oracle():  # discretize on a non-uniform grid (ieks.cpp:8-47)
     g = np.cumsum(np.concatenate([[0.0], 0.05 + 0.1 * np.abs(np.sin(np.arange(80)))]))
     got = P.para_ieks(P.van_der_pol(), P.IwpPrior(2, 2, 1.0), g)
