@@ -306,7 +306,13 @@ struct FastEngine {
     if (env && *env) return static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(std::atoll(env), std::max<int64_t>(N, 2))));
     const int64_t target = Pass::target_chunks(ctx);
     const int64_t L = (N + target - 1) / target;
-    return static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(L, 4096)));
+    // Floor of the chunk length: below one resident wave of chunks the lane
+    // passes are latency chains of L steps, so small grids take short chunks
+    // (FHN, ms per iteration, tools/small_n_chunks.py: N = 2^12 L = 2 0.219
+    // vs L = 8 0.260; 2^14 0.251 vs 0.282; 2^16 L = 8 best).  Group passes
+    // keep 8.
+    const int64_t lmin = Pass::kLane ? std::max<int64_t>(2, std::min<int64_t>(8, N / 8192)) : 8;
+    return static_cast<int>(std::max<int64_t>(lmin, std::min<int64_t>(L, 4096)));
   }
 
   static IeksResult run(pode_context* ctx, const host::Problem& p, const pode_prior& prior, const double* grid_h,

@@ -371,6 +371,29 @@ __device__ __forceinline__ void gather_y(const FastArgs& a, const LinPoint& lp, 
   for (int j = 0; j < d; ++j) y[j] = at_n ? lp.term[j * B] : lp.eta[(tt * D + j * B) * a.nchunks + cc];
 }
 
+// L1 prefetch of gather_y's addresses (node k = s + t of chunk c): issued a
+// step or two ahead, so the load that the register allocator sinks next to
+// its use (the field evaluation) hits L1 instead of HBM.  PODE_Y_PREFETCH=0
+// disables.
+#ifndef PODE_Y_PREFETCH
+#define PODE_Y_PREFETCH 1
+#endif
+template <int D, int d>
+__device__ __forceinline__ void prefetch_y(const FastArgs& a, const LinPoint& lp, int64_t c, int64_t t, int64_t k) {
+  if constexpr (PODE_Y_PREFETCH) {
+    constexpr int B = D / d;
+    if (k > a.N) return;
+    const bool at_n = k == a.N;
+    const bool wrap = t == a.L;
+    const int64_t cc = wrap ? c + 1 : c, tt = wrap ? 0 : t;
+#pragma unroll
+    for (int j = 0; j < d; ++j) {
+      const double* p = at_n ? lp.term + j * B : lp.eta + (tt * D + j * B) * a.nchunks + cc;
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+    }
+  }
+}
+
 template <int D>
 __device__ __forceinline__ void soa_st(const ElemSoA& s, int64_t c, int64_t t, const double (&E)[D][D],
                                        const double (&g)[D]) {
@@ -510,8 +533,9 @@ __global__ void PODE_LANE_BOUNDS k_lane_fwd_reduce(const FastArgs a, FastConst<D
     M::predict_cov(pc, C, cst.q, cm);
     // update at node k+1
     double ylin[d];  // (a one-step-ahead load costs pass A more in spills than it saves)
+    if (k + 1 < e) prefetch_y<D, d>(a, lp, c, k + 2 - s, k + 2);
     gather_y<D, d>(a, lp, c, k + 1 - s, k + 1, ylin);
-    const typename M::Lin lin = M::linearize(prob, ylin, a.ek0, prob.kind == 7 ? a.grid[k + 1] : 0.0);
+    const typename M::Lin lin = M::linearize(prob, ylin, a.ek0, gcur);  // t_{k+1} (only PODE_POLE reads it)
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
     const typename M::Upd u = M::update(lin, tn, cm);
     bad_sing |= u.singular;
@@ -742,8 +766,9 @@ __device__ __forceinline__ double fwd_down_chunk(const FastArgs& a, const FastCo
     double ylin[d];
 #pragma unroll
     for (int i = 0; i < d; ++i) ylin[i] = ynext[i];
+    if (k + 2 < e) prefetch_y<D, d>(a, lp, c, k + 3 - s, k + 3);
     if (k + 1 < e) gather_y<D, d>(a, lp, c, k + 2 - s, k + 2, ynext);
-    const typename M::Lin lin = M::linearize(prob, ylin, a.ek0, prob.kind == 7 ? a.grid[k + 1] : 0.0);
+    const typename M::Lin lin = M::linearize(prob, ylin, a.ek0, gcur);  // t_{k+1} (only PODE_POLE reads it)
     if (!lin.finite && bad_lin < 0) bad_lin = k + 1;
     const typename M::Upd u = M::update(lin, tn, cm);
     bad_sing |= u.singular;
