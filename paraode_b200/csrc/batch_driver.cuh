@@ -77,14 +77,17 @@ namespace lane {
 // after the nc L D body, one per IVP).
 template <int D>
 __global__ void k_eta_fill_batch(const double* mu0s, int64_t nc, int L, int64_t seg_chunks, int nseg, double* base) {
-  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  const int64_t total = nc * L * D;
-  if (i < total) {
-    const int64_t c = i % nc;
-    base[i] = mu0s[(c / seg_chunks) * D + (i / nc) % D];
-  } else if (i < total + int64_t(nseg) * D) {
-    base[i] = mu0s[i - total];
+  const int row = blockIdx.y;  // t * D + r; row L D: the node-N slots
+  if (row == L * D) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nseg * D; i += gridDim.x * blockDim.x)
+      base[nc * L * D + i] = mu0s[i];
+    return;
   }
+  const int r = row % D;
+  const unsigned sc = static_cast<unsigned>(seg_chunks);
+  double* dst = base + int64_t(row) * nc;
+  for (unsigned c = blockIdx.x * blockDim.x + threadIdx.x; c < unsigned(nc); c += gridDim.x * blockDim.x)
+    dst[c] = mu0s[(c / sc) * D + r];
 }
 }  // namespace lane
 
@@ -219,7 +222,7 @@ struct BatchEngine {
     a.m0s = m0s;
     a.active = active;
 
-    lane::k_eta_fill_batch<D><<<grid1(int64_t(eta_len)), kRedThreads, 0, st>>>(mu0s, nc, L, seg_chunks, nb, pair0);
+    lane::k_eta_fill_batch<D><<<lane::eta_fill_grid(nc, L, D), 256, 0, st>>>(mu0s, nc, L, seg_chunks, nb, pair0);
     note_launch(ctx, "fill");
     reset_error(ctx);
     // objective of the constant start (pass E on pair0 = iteration parity 0)

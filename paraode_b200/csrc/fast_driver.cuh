@@ -19,13 +19,22 @@ namespace pode {
 
 namespace lane {
 
-// eta (N+1 nodes, chunk-interleaved + node-N slot) <- mu0 at every node.
+// eta (N+1 nodes, chunk-interleaved + node-N slot) <- mu0 at every node:
+// row (t D + r) of the layout (blockIdx.y) holds mu0[r] for every chunk.
 template <int D>
 __global__ void k_eta_fill(const double* mu0, int64_t nc, int L, double* base) {
-  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  const int64_t total = nc * L * D;
-  if (i < total) base[i] = mu0[(i / nc) % D];
-  if (i < D) base[total + i] = mu0[i];
+  const int row = blockIdx.y;  // t * D + r, t < L; row L D: the node-N slot
+  const double v = mu0[row % D];
+  if (row == L * D) {
+    if (blockIdx.x == 0 && threadIdx.x < D) base[nc * L * D + threadIdx.x] = mu0[threadIdx.x];
+    return;
+  }
+  double* dst = base + int64_t(row) * nc;
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < nc; c += int64_t(gridDim.x) * blockDim.x)
+    dst[c] = v;
+}
+inline dim3 eta_fill_grid(int64_t nc, int L, int D) {
+  return dim3(static_cast<unsigned>(std::min<int64_t>((nc + 255) / 256, 64)), static_cast<unsigned>(L * D + 1));
 }
 
 // chunk-interleaved eta -> (N+1) x D row-major
@@ -103,7 +112,7 @@ struct LanePasses {
     });
   }
   static void fill(cudaStream_t st, const double* mu0, int64_t nc, int L, double* eta) {
-    lane::k_eta_fill<D><<<grid1(nc * L * D + D), kRedThreads, 0, st>>>(mu0, nc, L, eta);
+    lane::k_eta_fill<D><<<lane::eta_fill_grid(nc, L, D), 256, 0, st>>>(mu0, nc, L, eta);
   }
   static void rows(cudaStream_t st, const double* base, const double* term, int64_t N, int L, int64_t nc,
                    double* out) {
@@ -649,7 +658,7 @@ struct FastEngine {
       d2d(ctx, soa.term, sview(acc).g, D);
     };
 
-    lane::k_eta_fill<D><<<grid1(int64_t(padded) * D + D), kRedThreads, 0, st>>>(s.mu0, nc, L, eta_a);
+    lane::k_eta_fill<D><<<lane::eta_fill_grid(nc, L, D), 256, 0, st>>>(s.mu0, nc, L, eta_a);
     note_launch(ctx, "fill");
     reset_error(ctx);
     // objective of the constant start (ieks.cpp:147-148)
