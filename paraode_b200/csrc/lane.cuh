@@ -1150,27 +1150,40 @@ __global__ void __launch_bounds__(kLaneThreads, kBwdMinBlocks) k_lane_bwd_down(F
     double tn[B];
 #pragma unroll
     for (int i = 0; i < B; ++i) tn[i] = tei[i];  // T_{k+1}^-1
-    // prefetch of step k = e - 1
-    double En[D][D], gn[D], on[D];
-    if (e - 1 >= s) {
-      if (!kInitial) soa_ld<D>(elems, c, e - 1 - s, En, gn);
+    // Register prefetch of the next step's (E, g, eta_old) where two D x D
+    // blocks fit beside the recursion (D <= 7); at D = 8, 9 it spilled
+    // (632 B of stack at D = 8), so those load at the top of each step from
+    // the L2 lines prefetched below.
+    constexpr bool kRegPre = D * D <= 49;
+    constexpr int DP = kRegPre ? D : 1;
+    double En[DP][DP], gn[DP], on[DP];
+    if constexpr (kRegPre) {
+      if (e - 1 >= s) {
+        if (!kInitial) soa_ld<DP>(elems, c, e - 1 - s, En, gn);
 #pragma unroll
-      for (int r = 0; r < D; ++r) on[r] = eta_old[((e - 1 - s) * D + r) * nc + c];
+        for (int r = 0; r < D; ++r) on[r] = eta_old[((e - 1 - s) * D + r) * nc + c];
+      }
     }
     BwdGrid bg(a.grid, a.first, e - 1);
     for (int64_t k = e - 1; k >= s; --k) {
       double E[D][D], gk[D], oldk[D];
+      if constexpr (kRegPre) {
 #pragma unroll
-      for (int r = 0; r < D; ++r) {
-        gk[r] = gn[r];
-        oldk[r] = on[r];
+        for (int r = 0; r < D; ++r) {
+          gk[r] = gn[r];
+          oldk[r] = on[r];
 #pragma unroll
-        for (int j = 0; j < D; ++j) E[r][j] = En[r][j];
-      }
-      if (k - 1 >= s) {
-        if (!kInitial) soa_ld<D>(elems, c, k - 1 - s, En, gn);
+          for (int j = 0; j < D; ++j) E[r][j] = En[r][j];
+        }
+        if (k - 1 >= s) {
+          if (!kInitial) soa_ld<DP>(elems, c, k - 1 - s, En, gn);
 #pragma unroll
-        for (int r = 0; r < D; ++r) on[r] = eta_old[((k - 1 - s) * D + r) * nc + c];
+          for (int r = 0; r < D; ++r) on[r] = eta_old[((k - 1 - s) * D + r) * nc + c];
+        }
+      } else {
+        if (!kInitial) soa_ld<D>(elems, c, k - s, E, gk);
+#pragma unroll
+        for (int r = 0; r < D; ++r) oldk[r] = eta_old[((k - s) * D + r) * nc + c];
       }
       if (!kInitial && k - 2 >= s) {
         // L2 prefetch of step k-2 for the whole warp (its 32 chunks span <= 3
