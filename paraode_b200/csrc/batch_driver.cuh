@@ -235,7 +235,7 @@ struct BatchEngine {
 
     ScanTally tf, tr;
     auto body = [&](bool graph, cudaGraphConditionalHandle h) {
-      lane::k_lane_fwd_reduce<D, d, true><<<blocks(nc), kTh, 0, st>>>(a, cst, agg);
+      lane::k_lane_fwd_reduce<D, d, true><<<blocks(nc), kTh, lane::fwd_reduce_smem<D>(), st>>>(a, cst, agg);
       note_launch(ctx, "fast_fwd_reduce");
       tf = Engine<D>::scan_filtering_gauss(ctx, nc, agg, agg, FE::scan_fanin());
       lane::k_lane_fwd_down<D, d, false, true><<<blocks(nc), kTh, lane::fwd_down_smem<D>(), st>>>(
@@ -325,7 +325,7 @@ struct BatchEngine {
     f.it_dev = nullptr;
     f.active = nullptr;
     f.seg_it = it_b;
-    lane::k_lane_fwd_reduce<D, d, true><<<blocks(nc), kTh, 0, st>>>(f, cst, agg);
+    lane::k_lane_fwd_reduce<D, d, true><<<blocks(nc), kTh, lane::fwd_reduce_smem<D>(), st>>>(f, cst, agg);
     note_launch(ctx, "fast_fwd_reduce");
     const ScanTally tfin = Engine<D>::scan_filtering_gauss(ctx, nc, agg, agg, FE::scan_fanin());
     double* cf = ws.arr<double>("batch_cf", padded * D * D + size_t(nb) * D * D);

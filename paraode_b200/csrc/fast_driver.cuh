@@ -109,6 +109,14 @@ struct LanePasses {
       cuda_check(cudaFuncSetAttribute(lane::k_lane_fwd_down<D, d, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(lane::fwd_down_smem<D>())),
                  "pass C smem");
+      if constexpr (lane::fwd_reduce_smem<D>() > 0) {
+        cuda_check(cudaFuncSetAttribute(lane::k_lane_fwd_reduce<D, d, false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(lane::fwd_reduce_smem<D>())),
+                   "pass A smem");
+        cuda_check(cudaFuncSetAttribute(lane::k_lane_fwd_reduce<D, d, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(lane::fwd_reduce_smem<D>())),
+                   "pass A smem");
+      }
     });
   }
   static void fill(cudaStream_t st, const double* mu0, int64_t nc, int L, double* eta) {
@@ -119,7 +127,7 @@ struct LanePasses {
     lane::k_eta_rows<D><<<grid1((N + 1) * D), kRedThreads, 0, st>>>(base, term, N, L, nc, out);
   }
   static void fwd_reduce(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const FEd& agg) {
-    lane::k_lane_fwd_reduce<D, d><<<blocks(a.nchunks), lane::kLaneThreads, 0, st>>>(a, cst, agg);
+    lane::k_lane_fwd_reduce<D, d><<<blocks(a.nchunks), lane::kLaneThreads, lane::fwd_reduce_smem<D>(), st>>>(a, cst, agg);
   }
   static void fwd_down(cudaStream_t st, const FastArgs& a, const FastConst<D>& cst, const FEd& agg,
                        const lane::ElemSoA& soa, const SEd& bagg) {
@@ -679,7 +687,7 @@ struct FastEngine {
       reset_error(ctx);
       a.eta = eta_a;
       a.eta_term = term(eta_a);
-      lane::k_lane_fwd_reduce<D, d><<<lblocks, th, 0, st>>>(a, cst, agg);
+      lane::k_lane_fwd_reduce<D, d><<<lblocks, th, lane::fwd_reduce_smem<D>(), st>>>(a, cst, agg);
       note_launch(ctx, "fast_fwd_reduce");
       forward_exchange();
       const ScanTally tf = Engine<D>::scan_filtering_gauss(ctx, nc, agg, agg, scan_fanin());

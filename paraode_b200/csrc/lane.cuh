@@ -437,6 +437,17 @@ constexpr size_t fwd_down_smem() {
   return sizeof(double) * (D * D + D) * kLaneThreads;
 }
 
+// Pass A keeps the chunk's A (D x D) in per-thread shared-memory slots when
+// A, C and J together exceed the register file (D >= 8: 1 KB of spills).
+template <int D>
+constexpr bool fwd_reduce_a_smem() {
+  return D >= 8;
+}
+template <int D>
+constexpr size_t fwd_reduce_smem() {
+  return fwd_reduce_a_smem<D>() ? sizeof(double) * D * D * kLaneThreads : 0;
+}
+
 // A D x D matrix per node in the chunk-interleaved layout of ElemSoA::e.
 template <int D>
 __device__ __forceinline__ void mat_st(double* base, int64_t nc, int64_t c, int64_t t, const double (&m)[D][D]) {
@@ -499,12 +510,20 @@ __global__ void PODE_LANE_BOUNDS k_lane_fwd_reduce(const FastArgs a, FastConst<D
   const bool head = sp.cl == 0 && a.first;
   const int64_t s = sp.cl * a.L;
   const int64_t e = min(a.N, s + a.L);
-  double A[D][D], C[D][D], J[D][D], b[D], eta[D];
+  constexpr bool kAS = fwd_reduce_a_smem<D>();
+  extern __shared__ double smem_a[];
+  // A in registers, or (kAS) in this thread's conflict-free smem slots
+  double A[kAS ? 1 : D][kAS ? 1 : D];
+  auto sa = [&](int r, int j) -> double& { return smem_a[(r * D + j) * kLaneThreads + threadIdx.x]; };
+  double C[D][D], J[D][D], b[D], eta[D];
 #pragma unroll
   for (int r = 0; r < D; ++r) {
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      A[r][j] = (!head && r == j) ? 1.0 : 0.0;
+      if constexpr (kAS)
+        sa(r, j) = (!head && r == j) ? 1.0 : 0.0;
+      else
+        A[r][j] = (!head && r == j) ? 1.0 : 0.0;
       C[r][j] = 0.0;
       J[r][j] = 0.0;
     }
@@ -527,7 +546,27 @@ __global__ void PODE_LANE_BOUNDS k_lane_fwd_reduce(const FastArgs a, FastConst<D
     for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
     M::phi_coefs(ratio, pc);
     // predict
-    M::template phi_rows<D>(pc, A);
+    if constexpr (kAS) {  // A <- phi A one block of B rows at a time
+#pragma unroll
+      for (int blk = 0; blk < d; ++blk) {
+        double x[B][D];
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+#pragma unroll
+          for (int j = 0; j < D; ++j) x[i][j] = sa(blk * B + i, j);
+#pragma unroll
+        for (int i = 0; i < B; ++i)
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            double o = pc[i][i] * x[i][j];
+#pragma unroll
+            for (int i2 = i + 1; i2 < B; ++i2) o = fma(pc[i][i2], x[i2][j], o);
+            sa(blk * B + i, j) = o;
+          }
+      }
+    } else {
+      M::template phi_rows<D>(pc, A);
+    }
     M::phi_vec(pc, b);
     double cm[D][D];
     M::predict_cov(pc, C, cst.q, cm);
@@ -540,7 +579,21 @@ __global__ void PODE_LANE_BOUNDS k_lane_fwd_reduce(const FastArgs a, FastConst<D
     const typename M::Upd u = M::update(lin, tn, cm);
     bad_sing |= u.singular;
     double U[d][D], uu[d];
-    M::template h_rows<D>(lin, tn, A, U);
+    if constexpr (kAS) {  // h_rows on the smem rows cB and iB+1
+#pragma unroll
+      for (int i = 0; i < d; ++i) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) U[i][j] = (1.0 * tn[1]) * sa(i * B + 1, j);
+#pragma unroll
+        for (int c2 = 0; c2 < d; ++c2) {
+          const double coef = (-lin.jac[i][c2]) * tn[0];
+#pragma unroll
+          for (int j = 0; j < D; ++j) U[i][j] = fma(coef, sa(c2 * B, j), U[i][j]);
+        }
+      }
+    } else {
+      M::template h_rows<D>(lin, tn, A, U);
+    }
     M::h_vec(lin, tn, b, uu);
 #pragma unroll
     for (int i = 0; i < d; ++i) uu[i] -= lin.off[i];
@@ -550,7 +603,12 @@ __global__ void PODE_LANE_BOUNDS k_lane_fwd_reduce(const FastArgs a, FastConst<D
 #pragma unroll
       for (int i = 0; i < d; ++i) {
 #pragma unroll
-        for (int j = 0; j < D; ++j) A[r][j] = fma(-u.k[r][i], U[i][j], A[r][j]);
+        for (int j = 0; j < D; ++j) {
+          if constexpr (kAS)
+            sa(r, j) = fma(-u.k[r][i], U[i][j], sa(r, j));
+          else
+            A[r][j] = fma(-u.k[r][i], U[i][j], A[r][j]);
+        }
         b[r] = fma(-u.k[r][i], uu[i], b[r]);
       }
     }
@@ -607,7 +665,14 @@ __global__ void PODE_LANE_BOUNDS k_lane_fwd_reduce(const FastArgs a, FastConst<D
   }
   if (bad_lin >= 0) raise_error(a.err, bad_lin, kErrLinearization);
   if (bad_sing) raise_error(a.err, s, kErrSingular);
-  st_mat<D>(agg.a + c * D * D, A);
+  if constexpr (kAS) {
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+      for (int j = 0; j < D; ++j) agg.a[c * D * D + r * D + j] = sa(r, j);
+  } else {
+    st_mat<D>(agg.a + c * D * D, A);
+  }
   st_mat<D>(agg.c + c * D * D, C);
   st_mat<D>(agg.j + c * D * D, J);
 #pragma unroll
