@@ -126,3 +126,20 @@ def test_scan_error_names_the_element_range(reverse):
     with pytest.raises(O.OracleError) as e:
         O.combine_filtering(fe[36:37], fe[37:38])
     assert e.value.kind == "SingularFactorError"
+
+
+def test_fused_batch_linearization_error_and_recovery():
+    """A batch whose third member has its pole on node 48 raises the
+    reference's LinearizationError (time 0.75, iteration 1); the same
+    context then solves a clean batch at the oracle's iterates."""
+    grid = O.uniform_grid(1.0, 64)
+    bad = [P.pole(0.7501), P.pole(0.7502), P.pole(0.75), P.pole(0.7503)]
+    with pytest.raises(P.LinearizationError) as g:
+        P.para_ieks_fused_batch(bad, P.IwpPrior(2, 1, 1.0), grid)
+    assert g.value.time == 0.75 and g.value.index == 48 and g.value.iteration == 1
+    good = [P.pole(0.7501), P.pole(0.7502)]
+    got = P.para_ieks_fused_batch(good, P.IwpPrior(2, 1, 1.0), grid)
+    for p, r in zip((0.7501, 0.7502), got):
+        want = O.ieks(O.ProblemSpec(7, 1, 1.0, [0.0], [p]), 2, grid, mode=0)
+        assert r.iterations == want["iterations"]
+        assert np.max(np.abs(r.means - want["means"])) <= 1e-9 * max(1.0, np.abs(want["means"]).max())
