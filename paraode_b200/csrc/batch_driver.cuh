@@ -104,8 +104,12 @@ struct BatchEngine {
   static int chunk_len(pode_context* ctx, int64_t N, int nb) {
     if (ctx->opt_chunk > 0) return static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(ctx->opt_chunk, N)));
     const int64_t target = int64_t(ctx->sm_count) * 256;
-    const int64_t L = (N * nb + target - 1) / target;
-    return static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(std::max<int64_t>(L, 8), std::min<int64_t>(N, 4096))));
+    int64_t L = (N * nb + target - 1) / target;
+    L = std::max<int64_t>(L, 8);
+    // at most N / 128 steps per chunk, so an IVP spans whole lane blocks
+    // instead of padding most of one
+    L = std::min<int64_t>(L, std::max<int64_t>(2, N / kTh));
+    return static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(L, std::min<int64_t>(N, 4096))));
   }
 
   // T_0^-1 (k_node_scales' formula for node 0 from the first step, ieks.cpp:28-33).
