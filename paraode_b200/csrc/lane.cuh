@@ -371,12 +371,12 @@ __device__ __forceinline__ void gather_y(const FastArgs& a, const LinPoint& lp, 
   for (int j = 0; j < d; ++j) y[j] = at_n ? lp.term[j * B] : lp.eta[(tt * D + j * B) * a.nchunks + cc];
 }
 
-// L1 prefetch of gather_y's addresses (node k = s + t of chunk c): issued a
-// step or two ahead, so the load that the register allocator sinks next to
-// its use (the field evaluation) hits L1 instead of HBM.  PODE_Y_PREFETCH=0
-// disables.
+// Prefetch of gather_y's addresses (node k = s + t of chunk c) a step or two
+// ahead (PODE_Y_PREFETCH=1: L1, 2: L2 evict_last).  Off by default: FHN 2^20
+// ms per iteration, three interleaved runs each, 0.822 (off) vs 0.829 (L1)
+// vs 0.829 (L2) — the sunk load's latency is covered by the other warp.
 #ifndef PODE_Y_PREFETCH
-#define PODE_Y_PREFETCH 1
+#define PODE_Y_PREFETCH 0
 #endif
 template <int D, int d>
 __device__ __forceinline__ void prefetch_y(const FastArgs& a, const LinPoint& lp, int64_t c, int64_t t, int64_t k) {
@@ -389,7 +389,10 @@ __device__ __forceinline__ void prefetch_y(const FastArgs& a, const LinPoint& lp
 #pragma unroll
     for (int j = 0; j < d; ++j) {
       const double* p = at_n ? lp.term + j * B : lp.eta + (tt * D + j * B) * a.nchunks + cc;
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+      if constexpr (PODE_Y_PREFETCH == 2)
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+      else
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
     }
   }
 }
