@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, kGrpMinBlocks) k_grp_fwd_reduce(cons
   for (int j = 0; j < D; ++j) q[j] = cst.q[(r < D ? r : 0) * D + j];
   double tk[B], tki[B];
   LM::taus(a.grid, a.first, s, tk, tki);
+  double gcur = a.grid[s], gnext = a.grid[s + 1], hlast = 0.0;
   bool bad_sing = false;
   int64_t bad_lin = -1;
   // every group of a warp runs L steps (group ops synchronise the warp); a
@@ -228,7 +229,15 @@ __global__ void __launch_bounds__(kThreads, kGrpMinBlocks) k_grp_fwd_reduce(cons
     const bool act = s + t < e;
     const int64_t k = act ? s + t : e - 1;
     double tn[B], tni[B], ratio[B], pc[B][B];
-    LM::taus(a.grid, a.first, k + 1, tn, tni);
+    // h_{k+1} from node times loaded a step ahead (a step past the chunk's
+    // end repeats the last step's h)
+    const double h = act ? gnext - gcur : hlast;
+    hlast = h;
+    if (act) {
+      gcur = gnext;
+      if (k + 2 <= a.N) gnext = a.grid[k + 2];
+    }
+    LM::taus_h(h, tn, tni);
 #pragma unroll
     for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
     LM::phi_coefs(ratio, pc);
@@ -241,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, kGrpMinBlocks) k_grp_fwd_reduce(cons
     // update at node k+1
     double y[d];
     load_y<D, d>(a, lp, k + 1, y);
-    const typename LM::Lin lin = LM::linearize(a.prob, y, a.ek0, a.prob.kind == 7 ? a.grid[k + 1] : 0.0);
+    const typename LM::Lin lin = LM::linearize(a.prob, y, a.ek0, gcur);  // t_{k+1} (only PODE_POLE reads it)
     if (act && !lin.finite && bad_lin < 0) bad_lin = k + 1;
     const typename M::Upd u = M::update(g, lin, tn, cm);
     bad_sing |= act && u.singular;
@@ -336,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, kGrpMinBlocks) k_grp_fwd_down(const 
   for (int j = 0; j < D; ++j) q[j] = cst.q[rr * D + j];
   double tk[B], tki[B];
   LM::taus(a.grid, a.first, s, tk, tki);
+  double gcur = a.grid[s], gnext = a.grid[s + 1], hlast = 0.0;
   bool bad_sing = false;
   int64_t bad_lin = -1;
   Rw<D> EA = zeros<D>();
@@ -345,7 +355,15 @@ __global__ void __launch_bounds__(kThreads, kGrpMinBlocks) k_grp_fwd_down(const 
     const bool st_ok = act && okc;
     const int64_t k = act ? s + t : e - 1;
     double tn[B], tni[B], ratio[B], pc[B][B];
-    LM::taus(a.grid, a.first, k + 1, tn, tni);
+    // h_{k+1} from node times loaded a step ahead (a step past the chunk's
+    // end repeats the last step's h)
+    const double h = act ? gnext - gcur : hlast;
+    hlast = h;
+    if (act) {
+      gcur = gnext;
+      if (k + 2 <= a.N) gnext = a.grid[k + 2];
+    }
+    LM::taus_h(h, tn, tni);
 #pragma unroll
     for (int i = 0; i < B; ++i) ratio[i] = tk[i] * tni[i];
     LM::phi_coefs(ratio, pc);
@@ -387,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, kGrpMinBlocks) k_grp_fwd_down(const 
     // measurement update at node k+1
     double y[d];
     load_y<D, d>(a, lp, k + 1, y);
-    const typename LM::Lin lin = LM::linearize(a.prob, y, a.ek0, a.prob.kind == 7 ? a.grid[k + 1] : 0.0);
+    const typename LM::Lin lin = LM::linearize(a.prob, y, a.ek0, gcur);  // t_{k+1} (only PODE_POLE reads it)
     if (act && !lin.finite && bad_lin < 0) bad_lin = k + 1;
     const typename M::Upd u = M::update(g, lin, tn, cm);
     bad_sing |= act && u.singular;
