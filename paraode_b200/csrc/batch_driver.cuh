@@ -360,10 +360,10 @@ struct BatchEngine {
       r.converged = h_conv[b] != 0;
       r.trace.assign(h_trace.begin() + size_t(b) * max_it, h_trace.begin() + size_t(b) * max_it + h_it[b]);
       r.sigma_hat = std::sqrt(h_innov[b] / count) * prior.sigma;
-      r.stats.combines = (N - seg_real) + tf.combines / nb + N;
+      // this IVP's share of the scan tally (its chunk folds, 1 / nb of the
+      // shared aggregate scans, the finalize's smoothing scan)
+      r.stats.combines = (N - seg_real) + tf.combines / nb + N + (tfin.combines + ts.combines) / nb;
       r.stats.depth = int64_t(L) + tf.depth + int64_t(L) + tr.depth;
-      (void)tfin;
-      (void)ts;
     }
     return out;
   }
