@@ -292,9 +292,14 @@ def run_ours(args):
     cfg = P.IeksConfig()
     gather = P.torch_allgather() if shard else None
     device_exchange = shard and os.environ.get("PODE_BENCH_BACKEND", "nccl") == "nccl"
+    exchange = "host all-gather (torch.distributed)" if shard else None
     if device_exchange:  # ncclAllGather inside the library on device buffers: no host staging per exchange
-        P.torch_nccl_bind(ctx)
-        gather = None
+        try:
+            P.torch_nccl_bind(ctx)
+            gather = None
+            exchange = "in-library ncclAllGather on device buffers"
+        except Exception as e:  # keep the run measurable: the host all-gather path
+            print(f"bench: NCCL bind failed ({e!r}); using the host all-gather exchange", file=sys.stderr)
 
     def solve_device():
         ptr = [C.cast(C.c_void_p(t.data_ptr()), A.dptr) for t in out_dev]
@@ -433,12 +438,9 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{prob.name} d={d} IWP(q={nu}) D={D}, N=2^{args.log2n} uniform steps, "
                                    "IEKS to the reference stopping rule", "N": n, "iterations": iters,
-                       "converged": converged, "step_iterations_per_s": value * iters / world,
+                       "converged": converged, "step_iterations_per_s": value * iters,
                        "ms_per_iteration": ms / max(iters, 1), **oracle_counts(args.problem, nu, args.log2n),
-                       "parallelism": (f"time-axis shards x{world} (" +
-                                       ("in-library ncclAllGather of chunk aggregates on device buffers"
-                                        if device_exchange else "host all-gather callback") + ")")
-                                      if shard else f"replicas x{world}",
+                       "parallelism": f"time-axis shards x{world} ({exchange})" if shard else f"replicas x{world}",
                        "l2": "working set > L2 (126 MB) per solve"},
             "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof,
             "e2e": {"value": e2e, "unit": "time-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
