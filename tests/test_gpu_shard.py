@@ -77,6 +77,7 @@ def run_sharded(name, nu, steps, world, env=None):
     ("fhn", 2, 2000, 2, {}),
     ("vanderpol", 2, 999, 3, {"PODE_CHUNK": "5"}),
     ("rigidbody", 2, 3000, 4, {"PODE_CHUNK": "3"}),
+    ("vanderpol", 3, 600, 2, {"PODE_CHUNK": "4"}),  # D = 8: pass A's A in shared memory
     ("fhn", 2, 4001, 3, {"PODE_CHUNK": "2", "PODE_SCAN_FANIN": "2"}),
 ])
 def test_sharded_matches_sequential_oracle(name, nu, steps, world, env):
