@@ -136,3 +136,39 @@ def test_fused_batch_at_scale():
     same = [a.iterations == b.iterations for a, b in zip(single, got)]
     print(f"64 x FHN N=4096 to convergence: one at a time {1e3 * (t1 - t0):.1f} ms, "
           f"fused batch {1e3 * (t2 - t1):.1f} ms; equal iteration counts {sum(same)}/64")
+
+
+def test_device_outputs_through_the_c_abi():
+    """pode_ieks_batch with PODE_DEVICE reports: the arrays stay in HBM and
+    equal the host-report path."""
+    import ctypes as C
+    import torch
+    from paraode_b200 import _abi as A
+    probs = _fhn_sweep(3)
+    grid = P.uniform_grid(20.0, 500)
+    prior = P.IwpPrior(2, 2, 1.0)
+    host = P.para_ieks_fused_batch(probs, prior, grid)
+    ctx = P.Context()
+    n1, D, d = grid.shape[0], prior.state_dim, prior.dim
+    outs = [[torch.empty(shape, dtype=torch.float64, device="cuda") for shape in
+             ((n1, D), (n1, D, D), (n1, d), (n1, d, d))] for _ in probs]
+    traces = [np.zeros(100) for _ in probs]
+    reps = (A.IeksReport * len(probs))()
+    for i in range(len(probs)):
+        ptr = [C.cast(C.c_void_p(t.data_ptr()), A.dptr) for t in outs[i]]
+        reps[i] = A.IeksReport(ptr[0], ptr[1], ptr[2], ptr[3], traces[i].ctypes.data_as(A.dptr), 100,
+                               A.PODE_DEVICE, 0, 0, 0.0, A.ScanStats())
+    pr = (A.Problem * len(probs))(*[p._c() for p in probs])
+    prior_c = A.Prior(prior.nu, prior.dim, prior.sigma)
+    cfg = A.IeksConfig(100, 1e-13, 1e-9, 1e-6, 0)
+    st = A.Status()
+    g = np.ascontiguousarray(grid)
+    rc = ctx._lib.pode_ieks_batch(ctx.handle, pr, len(probs), C.byref(prior_c),
+                                  g.ctypes.data_as(A.dptr), n1, C.byref(cfg), reps, C.byref(st))
+    assert rc == 0, st.msg
+    torch.cuda.synchronize()
+    for i, h in enumerate(host):
+        assert reps[i].iterations == h.iterations and bool(reps[i].converged) == h.converged
+        np.testing.assert_array_equal(outs[i][0].cpu().numpy(), h.means)
+        np.testing.assert_array_equal(outs[i][1].cpu().numpy(), h.cov_sqrt)
+        assert reps[i].sigma_hat == h.sigma_hat
