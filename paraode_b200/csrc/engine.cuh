@@ -10,6 +10,8 @@
 // bitwise reproducible run to run; work is <= 2n combines.
 #pragma once
 
+#include <functional>
+
 #include <algorithm>
 #include <mutex>
 #include <cstdlib>
@@ -418,25 +420,34 @@ __global__ void __launch_bounds__(kThreads, kGroupMinBlocks) k_scan_reduce_loc(F
   FOps<D>::store(agg, c, g.r, okc, acc);
 }
 
-// out[k] (b, C only) = carry[k / L - 1] ⊗ loc[k]; chunk 0 copies loc.
+// out[k] (b, C only) = carry[k / L - 1] ⊗ loc[k]; chunk 0 copies loc, or
+// (fc: a time-axis shard's incoming Gaussian, b then C) is fc ⊗ loc[k].
 template <int D>
 __global__ void __launch_bounds__(kThreads, kGroupMinBlocks) k_scan_down_gauss(FEd loc, int64_t n, int L, FEd carry, FEd out,
-                                                              DevError* err) {
+                                                              DevError* err, const double* fc = nullptr) {
   extern __shared__ double smem[];
   const Grp<D> g = make_group<D>(smem);
   const int64_t k = group_index<D>(g);
   const bool ok = g.real() && k < n;
   const int64_t c = k / L;
   const bool first = c == 0;
+  const bool copy = first && fc == nullptr;  // block-uniform
   const FEl<D> e = FOps<D>::load(loc, k, g.r, ok);
-  const double bi = ld_ent<D>(carry.b, c - 1, g.r, ok && !first);
-  const Rw<D> ci = ld_row<D>(carry.c, c - 1, g.r, ok && !first);
+  double bi;
+  Rw<D> ci;
+  if (first) {
+    bi = (ok && fc) ? fc[g.r] : 0.0;
+    ci = ld_row<D>(fc ? fc + D : nullptr, 0, g.r, ok && fc);
+  } else {
+    bi = ld_ent<D>(carry.b, c - 1, g.r, ok);
+    ci = ld_row<D>(carry.c, c - 1, g.r, ok);
+  }
   double bo;
   Rw<D> co;
   const bool good = combine_gauss<D>(g, bi, ci, e, bo, co);
-  if (ok && !first && g.r == 0 && !good) raise_error(err, k, kErrSingular);
-  st_ent<D>(out.b, k, g.r, ok, first ? e.b : bo);
-  st_row<D>(out.c, k, g.r, ok, first ? e.c : co);
+  if (ok && !copy && g.r == 0 && !good) raise_error(err, k, kErrSingular);
+  st_ent<D>(out.b, k, g.r, ok, copy ? e.b : bo);
+  st_row<D>(out.c, k, g.r, ok, copy ? e.c : co);
 }
 
 // ------------------------------------- reverse mean-only scan (E = 0 tail) ---
@@ -683,7 +694,12 @@ struct Engine {
   // produced (into out.b / out.c).  k-ary tree with local prefixes: depth
   // (L-1) full combines per level up, ONE Gaussian-carry combine per level
   // down.
-  static void scan_gauss_rec(pode_context* ctx, FEd in, FEd out, int64_t n, int level, int L, ScanTally& t) {
+  // top(full, n): called once at the top level with its n full inclusive
+  // prefixes (a time-axis shard reads its local total there and sets the
+  // incoming carry fc before the down-sweeps run).
+  using TopHook = std::function<void(FEd full, int64_t n)>;
+  static void scan_gauss_rec(pode_context* ctx, FEd in, FEd out, int64_t n, int level, int L, ScanTally& t,
+                             const TopHook* hook = nullptr, const double* fc = nullptr) {
     DevError* err = reinterpret_cast<DevError*>(ctx->d_err);
     size_t sm = smem_bytes<D>();
     FEd loc = alloc<FOps<D>>(ctx, "gscan_loc_" + std::to_string(level), n);
@@ -704,9 +720,13 @@ struct Engine {
         while ((1 << depth) < std::min<int64_t>(n, G)) ++depth;
         t.depth += depth;
         t.combines += n * depth;
-        if (nb == 1) return;
-        scan_gauss_rec(ctx, agg, agg, nb, level + 1, L, t);
-        k_scan_down_gauss<D><<<blocks_for<D>(n), kThreads, smem_bytes<D>(), ctx->stream>>>(loc, n, G, agg, out, err);
+        if (nb == 1) {
+          top_fix(ctx, out, out, n, hook, fc);
+          return;
+        }
+        scan_gauss_rec(ctx, agg, agg, nb, level + 1, L, t, hook, fc);
+        k_scan_down_gauss<D><<<blocks_for<D>(n), kThreads, smem_bytes<D>(), ctx->stream>>>(loc, n, G, agg, out, err,
+                                                                                            fc);
         note_launch(ctx, "scan_g_down");
         t.combines += n - std::min<int64_t>(n, G);
         t.depth += 1;
@@ -731,9 +751,13 @@ struct Engine {
       while ((1 << depth) < std::min<int64_t>(n, G)) ++depth;
       t.depth += depth;
       t.combines += n * depth;
-      if (nb == 1) return;
-      scan_gauss_rec(ctx, agg, agg, nb, level + 1, L, t);
-      k_scan_down_gauss<D><<<blocks_for<D>(n), kThreads, smem_bytes<D>(), ctx->stream>>>(loc, n, G, agg, out, err);
+      if (nb == 1) {
+        top_fix(ctx, out, out, n, hook, fc);
+        return;
+      }
+      scan_gauss_rec(ctx, agg, agg, nb, level + 1, L, t, hook, fc);
+      k_scan_down_gauss<D><<<blocks_for<D>(n), kThreads, smem_bytes<D>(), ctx->stream>>>(loc, n, G, agg, out, err,
+                                                                                          fc);
       note_launch(ctx, "scan_g_down");
       t.combines += n - std::min<int64_t>(n, G);
       t.depth += 1;
@@ -747,6 +771,10 @@ struct Engine {
       note_launch(ctx, "scan_g_reduce");
       t.combines += n - 1;
       t.depth += n - 1;
+      if (hook != nullptr) {
+        top_fix(ctx, loc, out, n, hook, fc);
+        return;
+      }
       cuda_check(cudaMemcpyAsync(out.b, loc.b, sizeof(double) * D * n, cudaMemcpyDeviceToDevice, ctx->stream),
                  "gscan copy");
       cuda_check(cudaMemcpyAsync(out.c, loc.c, sizeof(double) * D * D * n, cudaMemcpyDeviceToDevice, ctx->stream),
@@ -759,14 +787,39 @@ struct Engine {
     note_launch(ctx, "scan_g_reduce");
     t.combines += n - nc;
     t.depth += L - 1;
-    scan_gauss_rec(ctx, agg, agg, nc, level + 1, L, t);
-    k_scan_down_gauss<D><<<blocks_for<D>(n), kThreads, sm, ctx->stream>>>(loc, n, L, agg, out, err);
+    scan_gauss_rec(ctx, agg, agg, nc, level + 1, L, t, hook, fc);
+    k_scan_down_gauss<D><<<blocks_for<D>(n), kThreads, sm, ctx->stream>>>(loc, n, L, agg, out, err, fc);
     note_launch(ctx, "scan_g_down");
     t.combines += n - std::min<int64_t>(n, L);
     t.depth += 1;
   }
 
-  static ScanTally scan_filtering_gauss(pode_context* ctx, int64_t n, FEd in, FEd out, int L) {
+  // Top of a hooked scan: the hook sees the full prefixes, then (shard
+  // carry fc) every top prefix becomes fc ⊗ prefix (b, C into out).
+  static void top_fix(pode_context* ctx, FEd full, FEd out, int64_t n, const TopHook* top, const double* fc) {
+    if (top == nullptr) return;
+    (*top)(full, n);
+    if (fc == nullptr && full.b == out.b) return;
+    k_scan_down_gauss<D><<<blocks_for<D>(n), kThreads, smem_bytes<D>(), ctx->stream>>>(
+        full, n, static_cast<int>(n), full, out, reinterpret_cast<DevError*>(ctx->d_err), fc);
+    note_launch(ctx, "scan_g_top");
+  }
+
+  // The Gaussian-carry scan of a time-axis shard whose first element is not
+  // Gaussian: the up-sweep's top total goes to `top` (the exchange), which
+  // writes the incoming carry to fc (b then C; nullptr on the first shard:
+  // its first element absorbed the prior); the down-sweeps then apply fc to
+  // the first block of every level.  Same depth as the single-device scan,
+  // no separate reduction of the aggregates.
+  static ScanTally scan_filtering_gauss_shard(pode_context* ctx, int64_t n, FEd io, int L, const TopHook& top,
+                                              const double* fc) {
+    set_gauss_attrs();
+    ScanTally t;
+    if (n >= 1) scan_gauss_rec(ctx, io, io, n, 0, L, t, &top, fc);
+    return t;
+  }
+
+  static void set_gauss_attrs() {
     set_smem();
     static OncePerDevice once;
     once([&] {
@@ -774,6 +827,10 @@ struct Engine {
       cudaFuncSetAttribute(k_scan_reduce_loc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
       cudaFuncSetAttribute(k_scan_down_gauss<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     });
+  }
+
+  static ScanTally scan_filtering_gauss(pode_context* ctx, int64_t n, FEd in, FEd out, int L) {
+    set_gauss_attrs();
     ScanTally t;
     if (n >= 1) scan_gauss_rec(ctx, in, out, n, 0, L, t);
     return t;

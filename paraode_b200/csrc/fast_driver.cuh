@@ -642,21 +642,20 @@ struct FastEngine {
     a.last = rank == R - 1 ? 1 : 0;
     a.carry = carry;
 
-    // forward exchange: agg[0] <- (t_0 ⊗ .. ⊗ t_{rank-1}) ⊗ agg[0]; carry = its (b, C)
-    auto forward_exchange = [&]() {
-      const FEd tot = Engine<D>::template reduce_total<FOps<D>>(ctx, agg, nc, "sh_fred_");
+    // forward exchange, at the top of the local aggregate scan's up-sweep:
+    // the local total (the last top prefix) is all-gathered, shard r folds
+    // t_0 ⊗ .. ⊗ t_{r-1} (Gaussian: t_0 absorbed the prior) into `carry`,
+    // and the scan's down-sweeps apply it (Engine::scan_filtering_gauss_shard;
+    // no separate reduction of the aggregates)
+    const typename Engine<D>::TopHook forward_top = [&](FEd full, int64_t ntop) {
       double* own = xf + size_t(R) * kFel;
-      fel_move(ctx, tot, 0, fview(own), 0);
+      fel_move(ctx, full, ntop - 1, fview(own), 0);
       gather(ctx, comm, own, kFel, xf);
       if (rank == 0) return;
       for (int i = 1; i < rank; ++i)
         Engine<D>::template combine_one<FOps<D>>(ctx, fview(xf), fview(xf + size_t(i) * kFel), fview(xf));
       d2d(ctx, carry, fview(xf).b, D);
       d2d(ctx, carry + D, fview(xf).c, D * D);
-      double* tmp = xf + size_t(R + 1) * kFel;
-      fel_move(ctx, agg, 0, fview(tmp), 0);
-      Engine<D>::template combine_one<FOps<D>>(ctx, fview(xf), fview(tmp), fview(tmp));
-      fel_move(ctx, fview(tmp), 0, agg, 0);
     };
     // backward exchange: bagg[nc-1] <- bagg[nc-1] ⊗ (t_{rank+1} ⊗ .. ⊗ t_{R-1});
     // the incoming smoothed mean at the halo node -> elems.term
@@ -699,8 +698,8 @@ struct FastEngine {
       a.eta_term = term(eta_a);
       lane::k_lane_fwd_reduce<D, d><<<lblocks, th, lane::fwd_reduce_smem<D>(), st>>>(a, cst, agg);
       note_launch(ctx, "fast_fwd_reduce");
-      forward_exchange();
-      const ScanTally tf = Engine<D>::scan_filtering_gauss(ctx, nc, agg, agg, scan_fanin());
+      const ScanTally tf = Engine<D>::scan_filtering_gauss_shard(ctx, nc, agg, scan_fanin(), forward_top,
+                                                                 rank == 0 ? nullptr : carry);
       lane::k_lane_fwd_down<D, d><<<lblocks, th, lane::fwd_down_smem<D>(), st>>>(a, cst, agg, soa, nullptr, nullptr,
                                                                                 nullptr, bagg);
       note_launch(ctx, "fast_fwd_down");
