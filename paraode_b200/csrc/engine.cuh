@@ -478,9 +478,11 @@ __global__ void __launch_bounds__(kThreads) k_mscan_reduce_loc(SEd x, int64_t n,
 
 // out.g[k] = loc[k] ⊗ (0, g_carry) = E_loc g_carry + g_loc, carry = the
 // suffix of the next chunk (the last chunk copies loc).
+// rc (a time-axis shard's smoothed mean at its right halo node): the last
+// chunk is E_loc rc + g_loc instead of a copy.
 template <int D>
 __global__ void __launch_bounds__(kThreads) k_mscan_down(SEd loc, int64_t n, int L, int64_t nchunks, SEd carry,
-                                                         SEd out) {
+                                                         SEd out, const double* rc = nullptr) {
   extern __shared__ double smem[];
   const Grp<D> g = make_group<D>(smem);
   const int64_t k = group_index<D>(g);
@@ -488,9 +490,9 @@ __global__ void __launch_bounds__(kThreads) k_mscan_down(SEd loc, int64_t n, int
   const int64_t c = k / L;
   const bool last = c >= nchunks - 1;
   const typename MOps<D>::El e = MOps<D>::load(loc, k, g.r, ok);
-  const double gc = ld_ent<D>(carry.g, c + 1, g.r, ok && !last);
+  const double gc = last ? ((ok && rc) ? rc[g.r] : 0.0) : ld_ent<D>(carry.g, c + 1, g.r, ok);
   const double go = matvec(g, e.e, gc) + e.g;
-  st_ent<D>(out.g, k, g.r, ok, last ? e.g : go);
+  st_ent<D>(out.g, k, g.r, ok, (last && rc == nullptr) ? e.g : go);
 }
 
 // IEKS chunk aggregates: C and J are tria outputs (lower triangular).
@@ -838,7 +840,20 @@ struct Engine {
 
   // Reverse inclusive scan of mean-only elements ending in the terminal
   // element (E = 0): only the suffix means (out.g) are produced.
-  static void mscan_rec(pode_context* ctx, SEd in, SEd out, int64_t n, int level, int L, ScanTally& t) {
+  // hook(full, n): called at the top level with its n full suffixes (a
+  // time-axis shard reads its local total, element 0, and writes its right
+  // carry rc before the down-sweeps run).
+  using MTopHook = std::function<void(SEd full, int64_t n)>;
+  static void mscan_top_fix(pode_context* ctx, SEd full, SEd out, int64_t n, const MTopHook* hook, const double* rc) {
+    if (hook == nullptr) return;
+    (*hook)(full, n);
+    if (rc == nullptr && full.g == out.g) return;
+    k_mscan_down<D><<<blocks_for<D>(n), kThreads, smem_bytes<D>(), ctx->stream>>>(full, n, static_cast<int>(n), 1,
+                                                                                  full, out, rc);
+    note_launch(ctx, "scan_m_top");
+  }
+  static void mscan_rec(pode_context* ctx, SEd in, SEd out, int64_t n, int level, int L, ScanTally& t,
+                        const MTopHook* hook = nullptr, const double* rc = nullptr) {
     size_t sm = smem_bytes<D>();
     SEd loc = alloc<SOps<D>>(ctx, "mscan_loc_" + std::to_string(level), n);
     if (level >= 1 && n <= bscan_max() && bscan_fits<D, MOps<D>>()) {  // block Sklansky levels
@@ -859,9 +874,12 @@ struct Engine {
       while ((1 << depth) < std::min<int64_t>(n, G)) ++depth;
       t.depth += depth;
       t.combines += n * depth;
-      if (nb == 1) return;
-      mscan_rec(ctx, agg, agg, nb, level + 1, L, t);
-      k_mscan_down<D><<<blocks_for<D>(n), kThreads, smem_bytes<D>(), ctx->stream>>>(loc, n, G, nb, agg, out);
+      if (nb == 1) {
+        mscan_top_fix(ctx, out, out, n, hook, rc);
+        return;
+      }
+      mscan_rec(ctx, agg, agg, nb, level + 1, L, t, hook, rc);
+      k_mscan_down<D><<<blocks_for<D>(n), kThreads, smem_bytes<D>(), ctx->stream>>>(loc, n, G, nb, agg, out, rc);
       note_launch(ctx, "scan_m_down");
       t.combines += n - std::min<int64_t>(n, G);
       t.depth += 1;
@@ -872,6 +890,10 @@ struct Engine {
       note_launch(ctx, "scan_m_reduce");
       t.combines += n - 1;
       t.depth += n - 1;
+      if (hook != nullptr) {
+        mscan_top_fix(ctx, loc, out, n, hook, rc);
+        return;
+      }
       cuda_check(cudaMemcpyAsync(out.g, loc.g, sizeof(double) * D * n, cudaMemcpyDeviceToDevice, ctx->stream),
                  "mscan copy");
       return;
@@ -882,22 +904,36 @@ struct Engine {
     note_launch(ctx, "scan_m_reduce");
     t.combines += n - nc;
     t.depth += L - 1;
-    mscan_rec(ctx, agg, agg, nc, level + 1, L, t);
-    k_mscan_down<D><<<blocks_for<D>(n), kThreads, sm, ctx->stream>>>(loc, n, L, nc, agg, out);
+    mscan_rec(ctx, agg, agg, nc, level + 1, L, t, hook, rc);
+    k_mscan_down<D><<<blocks_for<D>(n), kThreads, sm, ctx->stream>>>(loc, n, L, nc, agg, out, rc);
     note_launch(ctx, "scan_m_down");
     t.combines += n - std::min<int64_t>(n, L);
     t.depth += 1;
   }
 
-  static ScanTally scan_means_terminal(pode_context* ctx, int64_t n, SEd io, int L) {
+  static void set_mscan_attrs() {
     static OncePerDevice once;
     once([&] {
       const int bytes = static_cast<int>(smem_bytes<D>());
       cudaFuncSetAttribute(k_mscan_reduce_loc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
       cudaFuncSetAttribute(k_mscan_down<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     });
+  }
+  static ScanTally scan_means_terminal(pode_context* ctx, int64_t n, SEd io, int L) {
+    set_mscan_attrs();
     ScanTally t;
     if (n >= 1) mscan_rec(ctx, io, io, n, 0, L, t);
+    return t;
+  }
+  // A time-axis shard's mean scan: its last chunk does not hold the terminal
+  // element; `hook` gets the local total at the top (the exchange) and writes
+  // the right carry rc (nullptr on the last shard), which the down-sweeps
+  // apply to the last block of every level.
+  static ScanTally scan_means_terminal_shard(pode_context* ctx, int64_t n, SEd io, int L, const MTopHook& hook,
+                                             const double* rc) {
+    set_mscan_attrs();
+    ScanTally t;
+    if (n >= 1) mscan_rec(ctx, io, io, n, 0, L, t, &hook, rc);
     return t;
   }
 

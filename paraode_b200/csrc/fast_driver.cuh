@@ -657,21 +657,19 @@ struct FastEngine {
       d2d(ctx, carry, fview(xf).b, D);
       d2d(ctx, carry + D, fview(xf).c, D * D);
     };
-    // backward exchange: bagg[nc-1] <- bagg[nc-1] ⊗ (t_{rank+1} ⊗ .. ⊗ t_{R-1});
-    // the incoming smoothed mean at the halo node -> elems.term
-    auto backward_exchange = [&]() {
-      const SEd tot = Engine<D>::template reduce_total<MOps<D>>(ctx, bagg, nc, "sh_bred_");
+    // backward exchange, at the top of the local mean scan's up-sweep: the
+    // local (E, g) total is all-gathered, shard r folds t_{r+1} ⊗ .. ⊗
+    // t_{R-1} from the right (E = 0: the last shard absorbed the terminal)
+    // into the smoothed mean at its halo node (elems.term), which the scan's
+    // down-sweeps apply to its last block at every level
+    const typename Engine<D>::MTopHook backward_top = [&](SEd full, int64_t) {
       double* own = xs + size_t(R) * kSel;
-      sel_move(ctx, tot, 0, sview(own), 0, false);
+      sel_move(ctx, full, 0, sview(own), 0, false);
       gather(ctx, comm, own, kSel, xs);
       if (rank == R - 1) return;
       double* acc = xs + size_t(R - 1) * kSel;
       for (int i = R - 2; i > rank; --i)
         Engine<D>::template combine_one<MOps<D>>(ctx, sview(xs + size_t(i) * kSel), sview(acc), sview(acc));
-      double* tmp = xs + size_t(R + 1) * kSel;
-      sel_move(ctx, bagg, nc - 1, sview(tmp), 0, false);
-      Engine<D>::template combine_one<MOps<D>>(ctx, sview(tmp), sview(acc), sview(tmp));
-      sel_move(ctx, sview(tmp), 0, bagg, nc - 1, false);
       d2d(ctx, soa.term, sview(acc).g, D);
     };
 
@@ -703,8 +701,8 @@ struct FastEngine {
       lane::k_lane_fwd_down<D, d><<<lblocks, th, lane::fwd_down_smem<D>(), st>>>(a, cst, agg, soa, nullptr, nullptr,
                                                                                 nullptr, bagg);
       note_launch(ctx, "fast_fwd_down");
-      backward_exchange();
-      const ScanTally tr = Engine<D>::scan_means_terminal(ctx, nc, bagg, scan_fanin());
+      const ScanTally tr = Engine<D>::scan_means_terminal_shard(ctx, nc, bagg, scan_fanin(), backward_top,
+                                                                rank == R - 1 ? nullptr : soa.term);
       lane::k_lane_bwd_down<D, d, false><<<lblocks, th, 0, st>>>(a, cst, soa, bagg, eta_a, term(eta_a), eta_b,
                                                                   term(eta_b), part);
       note_launch(ctx, "fast_bwd_down");
